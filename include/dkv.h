@@ -1,0 +1,132 @@
+/*
+ * dkv.h -- C ABI of the B200 (sm_100a) DualKV attention library (libdkv.so).
+ *
+ * Plain pointers and sizes only: no torch / Python types cross this
+ * boundary.  Every entry point is stream-ordered on the caller's stream,
+ * never allocates device memory (the caller passes outputs and workspace),
+ * never throws, and returns DKV_OK (0) or a negative error class; the
+ * message of the last error on the calling thread is in dkv_last_error().
+ *
+ * Tensor layouts (all row-major, contiguous, device memory):
+ *   q, out, dout, dq      [total_q, heads,    head_dim]
+ *   k, v, dk, dv          [total_q, kv_heads, head_dim]   per-sequence keys
+ *   k_ctx, v_ctx, dk_ctx  [ctx_len, kv_heads, head_dim]   the ONE shared prompt copy
+ *   lse                   [heads, total_q] float32, natural log
+ *   cu_seqlens            [num_seqs + 1]   int32, cu[0] = 0, cu[N] = total_q
+ * Query row r of sequence i has logical position ctx_len + r; it sees every
+ * context key and its own keys 0..r.
+ *
+ * Reference interfaces each entry point replaces (paths under
+ * /root/reference/pkg/src/dualkv/):
+ *   dkv_dualkv_fwd      <- kernel.py:177-210  dualkv_fwd(DualKVInput) -> (O, lse)
+ *   dkv_dualkv_bwd      <- kernel.py:245-293  dualkv_bwd(inp, O, lse, dO, deterministic, fold_seed)
+ *                          (ctx_partials != NULL: kernel.py:296-305 context_grad_contributions)
+ *   dkv_varlen_fwd      <- fa2.py:237-265     fa2_varlen_fwd(VarlenBatch) -> (O, lse)
+ *   dkv_varlen_bwd      <- fa2.py:268-306     fa2_varlen_bwd(batch, O, lse, dO) -> (dQ, dK, dV)
+ *   dkv_convert_f32_to_bf16 <- kernel.py:140-148 convert_dkv_context (one RNE cast, tensor.py:39-58)
+ *   dkv_gather_rows / dkv_segment_sum_rows
+ *                       <- packing.py:159-220 pack_standard / pack_dualkv as a device
+ *                          repack of activations (and its adjoint for gradients)
+ */
+#ifndef DKV_H_
+#define DKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DKV_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define DKV_API __attribute__((visibility("default")))
+#else
+#define DKV_API
+#endif
+
+enum dkv_status {
+  DKV_OK = 0,
+  DKV_ERR_INVALID = -1,     /* contract violation (maps to ValueError) */
+  DKV_ERR_UNSUPPORTED = -2, /* legal input this build cannot run (maps to ValueError) */
+  DKV_ERR_CUDA = -3,        /* launch / driver failure (maps to RuntimeError) */
+  DKV_ERR_WORKSPACE = -4    /* workspace too small */
+};
+
+enum dkv_dtype { DKV_BF16 = 0, DKV_F32 = 1 };
+
+typedef struct dkv_fwd_params {
+  const void* q;
+  const void* k_ctx; /* may be NULL when ctx_len == 0 */
+  const void* v_ctx;
+  const void* k;
+  const void* v;
+  const int32_t* cu_seqlens;
+  void* out;
+  float* lse;
+  int64_t num_seqs, total_q, ctx_len, heads, kv_heads, head_dim;
+  int64_t max_seqlen; /* max_i R_i (bounds the launch grid; must be >= the true max) */
+  float softmax_scale;
+  int32_t dtype;      /* enum dkv_dtype */
+} dkv_fwd_params;
+
+typedef struct dkv_bwd_params {
+  const void* q;
+  const void* k_ctx;
+  const void* v_ctx;
+  const void* k;
+  const void* v;
+  const int32_t* cu_seqlens;
+  const void* out;   /* saved forward output */
+  const float* lse;  /* saved forward lse [heads, total_q] */
+  const void* dout;
+  void* dq;
+  void* dk_ctx;      /* shared-prompt gradients (NULL when ctx_len == 0) */
+  void* dv_ctx;
+  void* dk;
+  void* dv;
+  int64_t num_seqs, total_q, ctx_len, heads, kv_heads, head_dim, max_seqlen;
+  float softmax_scale;
+  int32_t dtype;
+  int32_t deterministic; /* 1: context fold in fixed chunk order (bitwise reproducible dK_c/dV_c) */
+  int32_t ctx_chunk;     /* sequences per context work unit; 0 = automatic */
+  float* ctx_partials;   /* optional [num_chunks, 2, ctx_len, kv_heads, head_dim] f32 output of the
+                            un-folded per-chunk context contributions (instrumentation hook) */
+} dkv_bwd_params;
+
+DKV_API int32_t dkv_abi_version(void);
+DKV_API const char* dkv_last_error(void);
+/* 1 when the tensor-core (tcgen05) path serves this shape/dtype, 0 when the SIMT path does. */
+DKV_API int32_t dkv_uses_tensor_cores(int32_t dtype, int64_t head_dim, int64_t heads, int64_t kv_heads);
+
+DKV_API int32_t dkv_dualkv_fwd(const dkv_fwd_params* p, void* stream);
+DKV_API int32_t dkv_varlen_fwd(const dkv_fwd_params* p, void* stream);
+
+/* Bytes of scratch dkv_*_bwd needs for these parameters (fp32 dQ accumulator,
+ * packed (lse, D) rows, fp32 shared-prompt accumulators or per-chunk partials). */
+DKV_API size_t dkv_bwd_workspace_size(const dkv_bwd_params* p);
+/* Number of context chunks the backward uses (rows of ctx_partials). */
+DKV_API int64_t dkv_bwd_num_ctx_chunks(const dkv_bwd_params* p);
+DKV_API int32_t dkv_dualkv_bwd(const dkv_bwd_params* p, void* workspace, size_t workspace_bytes, void* stream);
+DKV_API int32_t dkv_varlen_bwd(const dkv_bwd_params* p, void* workspace, size_t workspace_bytes, void* stream);
+
+/* dst[i] = RNE_bf16(src[i]), bit-identical to the reference bf16_round. */
+DKV_API int32_t dkv_convert_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
+
+/* dst[r, :] = src[idx[r], :] for r < n_rows; rows are row_bytes long (multiple of 16 fastest). */
+DKV_API int32_t dkv_gather_rows(const void* src, void* dst, int64_t row_bytes, const int64_t* idx,
+                        int64_t n_rows, void* stream);
+/* dst[r, :] = sum_{j in [seg[r], seg[r+1])} src[src_idx[j], :], fp32 accumulate, dtype storage. */
+DKV_API int32_t dkv_segment_sum_rows(const void* src, void* dst, int32_t dtype, int64_t row_elems,
+                             const int64_t* seg, const int64_t* src_idx, int64_t n_rows,
+                             void* stream);
+
+/* Self-test of the UMMA operand layouts used by the kernels (debug aid):
+ * 128x128 (or 128xN) bf16 product through TMA + tcgen05, D fp32 [128][N]. */
+DKV_API int32_t dkv_selftest_umma(int32_t mode, const void* a, const void* b, float* d, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DKV_H_ */

@@ -1,0 +1,24 @@
+"""B200-native (sm_100a) DualKV shared-prompt attention.
+
+Drop-in for the attention path of the reference CPU package `dualkv`
+(arxiv 2605.15422): the same public names and signatures, executed by
+hand-written tcgen05/TMEM/TMA kernels behind the C ABI of `libdkv.so`.
+"""
+
+from .api import (  # noqa: F401
+    ContextGradScratch,
+    DualKVInput,
+    VarlenBatch,
+    bf16_naive_accumulate,
+    context_grad_contributions,
+    convert_dkv_context,
+    dualkv_attention_varlen,
+    dualkv_bwd,
+    dualkv_fwd,
+    fa2_varlen_bwd,
+    fa2_varlen_fwd,
+    uses_tensor_cores,
+)
+from .costmodel import attention_flops, visible_pairs  # noqa: F401
+
+__version__ = "0.1.0"

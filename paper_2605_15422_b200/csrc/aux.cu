@@ -1,0 +1,204 @@
+// aux.cu -- HBM-bound helper kernels around the attention core:
+//   * backward preprocess: D = rowsum(dO * O) (fa2.py:232-234), in two layouts
+//   * fixed-order fold + single RNE cast of the shared-prompt gradient
+//     (kernel.py:279-285 / convert_dkv_context kernel.py:140-148)
+//   * f32 -> storage cast (dQ accumulator, generic convert)
+//   * row gather / segment-sum for the N(P+R) <-> P+NR repack (packing.py:159-220)
+#include "dkv_internal.h"
+
+namespace dkv {
+
+template <typename T>
+DKV_DEVICE float to_f(T v);
+template <>
+DKV_DEVICE float to_f<float>(float v) { return v; }
+template <>
+DKV_DEVICE float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// one warp per (token, head).  drow: [H][T] (may be null); dpack: [Hk][T][G] float2
+// (lse * log2(e), D) -- the row order the GQA-packed tensor-core tiles consume.
+template <typename T>
+__global__ void rowsum_kernel(SimtArgs a, float* drow, float* dpack) {
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= static_cast<int64_t>(a.total_q) * a.heads) return;
+  const int t = static_cast<int>(gw / a.heads), h = static_cast<int>(gw % a.heads);
+  const int64_t off = (static_cast<int64_t>(t) * a.heads + h) * a.head_dim;
+  const T* o = static_cast<const T*>(a.out) + off;
+  const T* g = static_cast<const T*>(a.dout) + off;
+  float acc = 0.f;
+  for (int e = lane; e < a.head_dim; e += 32) acc += to_f(o[e]) * to_f(g[e]);
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if (lane == 0) {
+    if (drow) drow[static_cast<int64_t>(h) * a.total_q + t] = acc;
+    if (dpack) {
+      const int G = a.heads / a.kv_heads;
+      const int hk = h / G, gi = h % G;
+      const int64_t idx = (static_cast<int64_t>(hk) * a.total_q + t) * G + gi;
+      const float lse = a.lse[static_cast<int64_t>(h) * a.total_q + t];
+      reinterpret_cast<float2*>(dpack)[idx] = make_float2(lse * 1.4426950408889634f, acc);
+    }
+  }
+}
+
+void launch_rowsum_do_o(const SimtArgs& a, float* drow, float* dpack, cudaStream_t st) {
+  const int64_t warps = static_cast<int64_t>(a.total_q) * a.heads;
+  if (warps == 0) return;
+  const int threads = 256;
+  const int64_t blocks = (warps * 32 + threads - 1) / threads;
+  if (a.dtype == DKV_F32)
+    rowsum_kernel<float><<<blocks, threads, 0, st>>>(a, drow, dpack);
+  else
+    rowsum_kernel<__nv_bfloat16><<<blocks, threads, 0, st>>>(a, drow, dpack);
+}
+
+// dk/dv[i] = cast(sum_{c < num_parts} partials[c][0/1][i]), fixed chunk order
+__global__ void fold_convert_kernel(const float* __restrict__ parts, int num_parts, int64_t plane, void* dk,
+                                    void* dv, int dtype) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= 2 * plane) return;
+  const int which = static_cast<int>(i / plane);
+  const int64_t e = i % plane;
+  float acc = 0.f;
+  for (int c = 0; c < num_parts; ++c) acc += parts[(static_cast<int64_t>(c) * 2 + which) * plane + e];
+  void* dst = which == 0 ? dk : dv;
+  if (dtype == DKV_F32)
+    static_cast<float*>(dst)[e] = acc;
+  else
+    static_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(acc);
+}
+
+void launch_fold_convert(const float* partials, int num_parts, int64_t plane, void* dk, void* dv, int dtype,
+                         cudaStream_t st) {
+  if (plane == 0) return;
+  const int threads = 256;
+  const int64_t blocks = (2 * plane + threads - 1) / threads;
+  fold_convert_kernel<<<blocks, threads, 0, st>>>(partials, num_parts, plane, dk, dv, dtype);
+}
+
+// vectorised f32 -> {bf16, f32}; RNE via __float2bfloat16_rn (== reference bf16_round)
+__global__ void convert_kernel(const float* __restrict__ src, void* dst, int dtype, int64_t n) {
+  const int64_t i4 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (i4 >= n) return;
+  if (i4 + 4 <= n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    float4 v = *reinterpret_cast<const float4*>(src + i4);
+    if (dtype == DKV_F32) {
+      float* d = static_cast<float*>(dst) + i4;
+      d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+    } else {
+      __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(dst) + i4);
+      d[0] = __floats2bfloat162_rn(v.x, v.y);
+      d[1] = __floats2bfloat162_rn(v.z, v.w);
+    }
+    return;
+  }
+  for (int64_t i = i4; i < n && i < i4 + 4; ++i) {
+    if (dtype == DKV_F32)
+      static_cast<float*>(dst)[i] = src[i];
+    else
+      static_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(src[i]);
+  }
+}
+
+void launch_convert(const float* src, void* dst, int dtype, int64_t n, cudaStream_t st) {
+  if (n == 0) return;
+  const int threads = 256;
+  const int64_t blocks = ((n + 3) / 4 + threads - 1) / threads;
+  convert_kernel<<<blocks, threads, 0, st>>>(src, dst, dtype, n);
+}
+
+// ---------------------------------------------------------------- repack
+// one CTA-slice per destination row; 16-byte vectors when rows allow it
+__global__ void gather_rows_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                   int64_t row_bytes, const int64_t* __restrict__ idx, int64_t n_rows) {
+  const int64_t r = blockIdx.x;
+  if (r >= n_rows) return;
+  const uint8_t* s = src + idx[r] * row_bytes;
+  uint8_t* d = dst + r * row_bytes;
+  if ((row_bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    const int64_t n16 = row_bytes >> 4;
+    for (int64_t i = threadIdx.x; i < n16; i += blockDim.x)
+      reinterpret_cast<int4*>(d)[i] = __ldg(reinterpret_cast<const int4*>(s) + i);
+  } else {
+    for (int64_t i = threadIdx.x; i < row_bytes; i += blockDim.x) d[i] = s[i];
+  }
+}
+
+template <typename T>
+__global__ void segment_sum_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t row_elems,
+                                   const int64_t* __restrict__ seg, const int64_t* __restrict__ sidx,
+                                   int64_t n_rows) {
+  const int64_t r = blockIdx.x;
+  if (r >= n_rows) return;
+  const int64_t j0 = seg[r], j1 = seg[r + 1];
+  for (int64_t e = threadIdx.x; e < row_elems; e += blockDim.x) {
+    float acc = 0.f;
+    for (int64_t j = j0; j < j1; ++j) acc += to_f(src[sidx[j] * row_elems + e]);
+    if constexpr (sizeof(T) == 4)
+      dst[r * row_elems + e] = acc;
+    else
+      dst[r * row_elems + e] = __float2bfloat16_rn(acc);
+  }
+}
+
+}  // namespace dkv
+
+using namespace dkv;
+
+extern "C" int32_t dkv_gather_rows(const void* src, void* dst, int64_t row_bytes, const int64_t* idx,
+                                   int64_t n_rows, void* stream) {
+  if (n_rows < 0 || row_bytes <= 0 || (n_rows > 0 && (!src || !dst || !idx))) {
+    set_error("dkv_gather_rows: invalid arguments");
+    return DKV_ERR_INVALID;
+  }
+  if (n_rows == 0) return DKV_OK;
+  const int threads = row_bytes >= 4096 ? 256 : 128;
+  gather_rows_kernel<<<static_cast<unsigned>(n_rows), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), row_bytes, idx, n_rows);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("dkv_gather_rows: ") + cudaGetErrorString(e));
+    return DKV_ERR_CUDA;
+  }
+  return DKV_OK;
+}
+
+extern "C" int32_t dkv_segment_sum_rows(const void* src, void* dst, int32_t dtype, int64_t row_elems,
+                                        const int64_t* seg, const int64_t* src_idx, int64_t n_rows,
+                                        void* stream) {
+  if (n_rows < 0 || row_elems <= 0 || (dtype != DKV_BF16 && dtype != DKV_F32)) {
+    set_error("dkv_segment_sum_rows: invalid arguments");
+    return DKV_ERR_INVALID;
+  }
+  if (n_rows == 0) return DKV_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  if (dtype == DKV_F32)
+    segment_sum_kernel<float><<<static_cast<unsigned>(n_rows), 128, 0, st>>>(
+        static_cast<const float*>(src), static_cast<float*>(dst), row_elems, seg, src_idx, n_rows);
+  else
+    segment_sum_kernel<__nv_bfloat16><<<static_cast<unsigned>(n_rows), 128, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(src), static_cast<__nv_bfloat16*>(dst), row_elems, seg, src_idx,
+        n_rows);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("dkv_segment_sum_rows: ") + cudaGetErrorString(e));
+    return DKV_ERR_CUDA;
+  }
+  return DKV_OK;
+}
+
+extern "C" int32_t dkv_convert_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!src || !dst))) {
+    set_error("dkv_convert_f32_to_bf16: invalid arguments");
+    return DKV_ERR_INVALID;
+  }
+  launch_convert(src, dst, DKV_BF16, n, static_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("dkv_convert_f32_to_bf16: ") + cudaGetErrorString(e));
+    return DKV_ERR_CUDA;
+  }
+  return DKV_OK;
+}

@@ -1,0 +1,390 @@
+// fwd_sm100.cu -- tcgen05/TMEM/TMA forward for DualKV attention (paths 1 & 2).
+//
+// One kernel serves
+//   * Call 2, the fused two-region DualKV forward (kernel.py:177-210): each
+//     query tile walks its own causal response tiles, then the shared-prompt
+//     tiles (no mask except the partial last tile), carrying one online
+//     softmax state across the region boundary and writing lse;
+//   * Call 1 / the replicated N-copy baseline (fa2.py:237-265): ctx_len == 0.
+//
+// Tiling (B200-first, not the reference's loop nest):
+//   * GQA packing: the G query heads sharing a KV head are packed into the MMA
+//     M dimension -- a 128-row Q tile is (128/G tokens) x (G heads), loaded by
+//     ONE 3-D TMA box straight from the [T, H, d] tensor.  Each K/V tile is
+//     read once for all G heads (the reference expands K/V with np.repeat,
+//     fa2.py:105-109).
+//   * Each CTA owns two Q tiles (A, B) of consecutive tokens and ping-pongs the
+//     tensor core between them: S_A = Q_A K^T and S_B = Q_B K^T share one K
+//     tile in smem; P is written back to TMEM as bf16 (aliasing S) and
+//     O += P V runs as a TS-MMA with A from TMEM.
+//   * TMEM: S_A [0,128) S_B [128,256) O_A [256,256+d) O_B [384,384+d) columns.
+//   * Online softmax in the log2 domain, one query row per thread (TMEM lane),
+//     with lazy O rescaling (only when the running max grows by > 8).
+//   * Roles: warps 0-3 softmax(A), 4-7 softmax(B), 8 TMA producer + TMEM
+//     allocator, 9 MMA issuer.
+#include "dkv_internal.h"
+#include "tma_host.h"
+
+namespace dkv {
+namespace fwd {
+
+constexpr int kBM = 128;  // rows per Q tile
+constexpr int kBN = 128;  // keys per KV tile
+constexpr int kThreads = 320;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+template <int D>
+struct Cfg {
+  static constexpr int kPanels = D / 64;
+  static constexpr int kTileBytes = kBM * D * 2;   // Q, K or V tile (bf16)
+  static constexpr int kPanelBytes = kBM * 128;    // one 64-column SW128 panel of 128 rows
+  static constexpr int kStages = D == 128 ? 2 : 3; // K ring and V ring depth
+  static constexpr int kSmemTiles = (2 + 2 * kStages) * kTileBytes;
+  static constexpr int kSmemBytes = kSmemTiles + 1024 /*barriers*/ + 1024 /*align slack*/;
+};
+
+struct Params {
+  CUtensorMap tm_q, tm_k, tm_v, tm_kc, tm_vc;
+  __nv_bfloat16* out;
+  float* lse;
+  const int32_t* cu;
+  int num_seqs, total_q, ctx_len, heads, kv_heads, group, tq, blocks_per_seq_max;
+  float scale_log2;  // softmax_scale * log2(e)
+};
+
+struct Smem {
+  uint64_t q_full;
+  uint64_t k_full[4], k_empty[4], v_full[4], v_empty[4];
+  uint64_t s_full[2], p_full[2], o_full[2];
+  uint32_t tmem_base;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_constant__ Params p) {
+  using C = Cfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ[2] = {base, base + C::kTileBytes};
+  uint8_t* sK = base + 2 * C::kTileBytes;
+  uint8_t* sV = sK + C::kStages * C::kTileBytes;
+  Smem& sm = *reinterpret_cast<Smem*>(base + C::kSmemTiles);
+
+  // ---- work item: (q-block pair counted from the sequence end, sequence, kv head)
+  const int hk = blockIdx.x % p.kv_heads;
+  const int rest = blockIdx.x / p.kv_heads;
+  const int seq = rest % p.num_seqs;
+  const int jb = rest / p.num_seqs;
+  const int seq0 = p.cu[seq];
+  const int rlen = p.cu[seq + 1] - seq0;
+  const int pair_tok = 2 * p.tq;
+  const int nblk = (rlen + pair_tok - 1) / pair_tok;
+  if (jb >= nblk) return;
+  const int tok0 = (nblk - 1 - jb) * pair_tok;  // first token of tile A (sequence-local)
+  const bool has_b = tok0 + p.tq < rlen;
+  const int last_tok = min(tok0 + pair_tok, rlen) - 1;
+  const int n_own = last_tok / kBN + 1;
+  const int n_ctx = (p.ctx_len + kBN - 1) / kBN;
+  const int n_iter = n_own + n_ctx;
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.q_full, 1);
+    for (int i = 0; i < C::kStages; ++i) {
+      mbar_init(&sm.k_full[i], 1);
+      mbar_init(&sm.k_empty[i], 1);
+      mbar_init(&sm.v_full[i], 1);
+      mbar_init(&sm.v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.s_full[i], 1);
+      mbar_init(&sm.p_full[i], 128);
+      mbar_init(&sm.o_full[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 8) tmem_alloc<512>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  // iteration -> (is_ctx, tile index); own tiles from the diagonal down, then context
+  auto tile_of = [&](int it, bool& is_ctx) {
+    if (it < n_own) {
+      is_ctx = false;
+      return n_own - 1 - it;
+    }
+    is_ctx = true;
+    return n_ctx - 1 - (it - n_own);
+  };
+
+  if (warp == 8) {
+    // ================= TMA producer
+    if (elect_one()) {
+      tma_prefetch(&p.tm_q);
+      tma_prefetch(&p.tm_k);
+      tma_prefetch(&p.tm_v);
+      if (n_ctx > 0) {
+        tma_prefetch(&p.tm_kc);
+        tma_prefetch(&p.tm_vc);
+      }
+      const uint64_t pol_kv = policy_evict_last();
+      const int qbytes = C::kPanelBytes * C::kPanels * (has_b ? 2 : 1);
+      mbar_arrive_expect_tx(&sm.q_full, qbytes);
+      for (int t = 0; t < (has_b ? 2 : 1); ++t)
+        for (int pn = 0; pn < C::kPanels; ++pn)
+          tma_load_3d(sQ[t] + pn * C::kPanelBytes, &p.tm_q, &sm.q_full, pn * 64, hk * p.group,
+                      seq0 + tok0 + t * p.tq);
+      for (int it = 0; it < n_iter; ++it) {
+        bool is_ctx;
+        const int j = tile_of(it, is_ctx);
+        const int slot = it % C::kStages;
+        const uint32_t ph = (it / C::kStages) & 1;
+        const CUtensorMap* mk = is_ctx ? &p.tm_kc : &p.tm_k;
+        const CUtensorMap* mv = is_ctx ? &p.tm_vc : &p.tm_v;
+        const int row = is_ctx ? j * kBN : seq0 + j * kBN;
+        mbar_wait(&sm.k_empty[slot], ph ^ 1);
+        mbar_arrive_expect_tx(&sm.k_full[slot], C::kTileBytes);
+        for (int pn = 0; pn < C::kPanels; ++pn)
+          tma_load_3d_hint(sK + slot * C::kTileBytes + pn * C::kPanelBytes, mk, &sm.k_full[slot], pn * 64, hk,
+                           row, pol_kv);
+        mbar_wait(&sm.v_empty[slot], ph ^ 1);
+        mbar_arrive_expect_tx(&sm.v_full[slot], C::kTileBytes);
+        for (int pn = 0; pn < C::kPanels; ++pn)
+          tma_load_3d_hint(sV + slot * C::kTileBytes + pn * C::kPanelBytes, mv, &sm.v_full[slot], pn * 64, hk,
+                           row, pol_kv);
+      }
+    }
+  } else if (warp == 9) {
+    // ================= MMA issuer (one thread)
+    if (elect_one()) {
+      const uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, false, false);
+      const uint32_t idesc_o = idesc_bf16_f32(kBM, D, false, true);
+      const uint32_t tS[2] = {tmem + 0, tmem + 128};
+      const uint32_t tO[2] = {tmem + 256, tmem + 256 + 128};
+      const int ntile = has_b ? 2 : 1;
+      auto issue_s = [&](int t, int kslot) {
+        const uint32_t qa = smem_u32(sQ[t]);
+        const uint32_t ka = smem_u32(sK + kslot * C::kTileBytes);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * C::kPanelBytes + (k & 3) * 32;
+          mma_ss(tS[t], sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + off, 16, 1024), idesc_s, k > 0);
+        }
+      };
+      auto issue_pv = [&](int t, int vslot, bool accum) {
+        const uint32_t va = smem_u32(sV + vslot * C::kTileBytes);
+#pragma unroll
+        for (int k = 0; k < kBN / 16; ++k)
+          mma_ts(tO[t], tS[t] + k * 8, sdesc_sw128(va + k * 2048, C::kPanelBytes, 1024), idesc_o,
+                 (accum || k > 0) ? 1u : 0u);
+      };
+      mbar_wait(&sm.q_full, 0);
+      mbar_wait(&sm.k_full[0], 0);
+      tc_fence_after();
+      for (int t = 0; t < ntile; ++t) {
+        issue_s(t, 0);
+        mma_commit(&sm.s_full[t]);
+      }
+      mma_commit(&sm.k_empty[0]);
+      for (int it = 0; it < n_iter; ++it) {
+        const int vslot = it % C::kStages;
+        const uint32_t vph = (it / C::kStages) & 1;
+        const int nslot = (it + 1) % C::kStages;
+        const uint32_t nph = ((it + 1) / C::kStages) & 1;
+        const bool more = it + 1 < n_iter;
+        mbar_wait(&sm.v_full[vslot], vph);
+        if (more) mbar_wait(&sm.k_full[nslot], nph);
+        for (int t = 0; t < ntile; ++t) {
+          mbar_wait(&sm.p_full[t], it & 1);
+          tc_fence_after();
+          issue_pv(t, vslot, it > 0);
+          if (t == ntile - 1) mma_commit(&sm.v_empty[vslot]);
+          if (more) {
+            issue_s(t, nslot);
+            mma_commit(&sm.s_full[t]);
+            if (t == ntile - 1) mma_commit(&sm.k_empty[nslot]);
+          } else {
+            mma_commit(&sm.o_full[t]);
+          }
+        }
+      }
+    }
+  } else {
+    // ================= softmax warpgroups: thread = one row of Q tile `t`
+    const int t = warp >> 2;
+    const int row = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane_off + t * 128;
+    const uint32_t tO = tmem + lane_off + 256 + t * 128;
+    const bool tile_ok = (t == 0) || has_b;
+    const int qtok = tok0 + t * p.tq + row / p.group;  // sequence-local token of this row
+    const int head = hk * p.group + row % p.group;
+    const bool row_valid = tile_ok && qtok < rlen;
+    const int qmin = tok0 + t * p.tq;                  // first token of the tile
+    float m_run = -INFINITY, l_run = 0.f;
+    if (tile_ok) {
+      for (int it = 0; it < n_iter; ++it) {
+        bool is_ctx;
+        const int j = tile_of(it, is_ctx);
+        mbar_wait(&sm.s_full[t], it & 1);
+        tc_fence_after();
+        float s[kBN];
+        {
+          uint32_t u[kBN];
+#pragma unroll
+          for (int c = 0; c < kBN / 32; ++c)
+            tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&u[c * 32]));
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < kBN; ++i) s[i] = __uint_as_float(u[i]);
+        }
+        // masks: own tiles on/after the tile's first token are causal; the last
+        // context tile may be partial (keys >= P are out of bounds)
+        const int kbase = j * kBN;
+        const bool need_mask = is_ctx ? (kbase + kBN > p.ctx_len) : (kbase + kBN - 1 > qmin);
+        if (need_mask) {
+          const int lim = is_ctx ? p.ctx_len - 1 - kbase : qtok - kbase;  // last visible column
+#pragma unroll
+          for (int c = 0; c < kBN; ++c)
+            if (c > lim) s[c] = -INFINITY;
+        }
+        float mx = s[0];
+#pragma unroll
+        for (int c = 1; c < kBN; ++c) mx = fmaxf(mx, s[c]);
+        const float m_tile = mx * p.scale_log2;
+        const float m_new = fmaxf(m_run, m_tile);
+        float alpha = 1.f;
+        if (m_new > m_run + kRescaleThreshold) {
+          alpha = ex2(m_run - m_new);
+          m_run = m_new;
+        }
+        const float m_use = m_run == -INFINITY ? 0.f : m_run;
+        float rowsum = 0.f;
+#pragma unroll
+        for (int c0 = 0; c0 < kBN; c0 += 32) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float e0 = ex2(fmaf(s[c0 + 2 * i], p.scale_log2, -m_use));
+            const float e1 = ex2(fmaf(s[c0 + 2 * i + 1], p.scale_log2, -m_use));
+            rowsum += e0 + e1;
+            pk[i] = pack_bf16(e0, e1);
+          }
+          tmem_st16(tS + c0 / 2, pk);
+        }
+        l_run = l_run * alpha + rowsum;
+        // O holds P V of iterations < it (its MMA completed before S(it) did)
+        if (it > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tO + c0, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            tmem_st32(tO + c0, r);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&sm.p_full[t]);
+      }
+      // ---- epilogue: O / l -> bf16, lse
+      mbar_wait(&sm.o_full[t], 0);
+      tc_fence_after();
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      __nv_bfloat16* orow = p.out + (static_cast<int64_t>(seq0 + qtok) * p.heads + head) * D;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tO + c0, r);
+        tmem_wait_ld();
+        if (row_valid) {
+          uint4 v[4];
+          uint32_t* w = reinterpret_cast<uint32_t*>(v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            w[i] = pack_bf16(__uint_as_float(r[2 * i]) * inv, __uint_as_float(r[2 * i + 1]) * inv);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dst[i] = v[i];
+        }
+      }
+      if (row_valid)
+        p.lse[static_cast<int64_t>(head) * p.total_q + seq0 + qtok] =
+            (m_run + __log2f(l_run)) * 0.6931471805599453f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int D>
+int launch(const SimtArgs& a, cudaStream_t st) {
+  using C = Cfg<D>;
+  Params p{};
+  const int G = a.heads / a.kv_heads;
+  const int tq = kBM / G;
+  if (!make_map_3d_bf16(&p.tm_q, a.q, a.total_q, a.heads, D, G, tq) ||
+      !make_map_3d_bf16(&p.tm_k, a.k, a.total_q, a.kv_heads, D, 1, kBN) ||
+      !make_map_3d_bf16(&p.tm_v, a.v, a.total_q, a.kv_heads, D, 1, kBN)) {
+    set_error("cuTensorMapEncodeTiled failed for q/k/v");
+    return DKV_ERR_CUDA;
+  }
+  if (a.ctx_len > 0) {
+    if (!make_map_3d_bf16(&p.tm_kc, a.k_ctx, a.ctx_len, a.kv_heads, D, 1, kBN) ||
+        !make_map_3d_bf16(&p.tm_vc, a.v_ctx, a.ctx_len, a.kv_heads, D, 1, kBN)) {
+      set_error("cuTensorMapEncodeTiled failed for k_ctx/v_ctx");
+      return DKV_ERR_CUDA;
+    }
+  }
+  p.out = static_cast<__nv_bfloat16*>(a.out);
+  p.lse = a.lse;
+  p.cu = a.cu;
+  p.num_seqs = a.num_seqs;
+  p.total_q = a.total_q;
+  p.ctx_len = a.ctx_len;
+  p.heads = a.heads;
+  p.kv_heads = a.kv_heads;
+  p.group = G;
+  p.tq = tq;
+  p.scale_log2 = a.scale * 1.4426950408889634f;
+  const int blocks_per_seq = (a.max_seqlen + 2 * tq - 1) / (2 * tq);
+  const int64_t grid = static_cast<int64_t>(blocks_per_seq) * a.num_seqs * a.kv_heads;
+  if (grid == 0) return DKV_OK;
+  if (grid > 0x7fffffff) {
+    set_error("forward grid too large");
+    return DKV_ERR_UNSUPPORTED;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(dualkv_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    attr_set = true;
+  }
+  dualkv_fwd_kernel<D><<<static_cast<unsigned>(grid), kThreads, C::kSmemBytes, st>>>(p);
+  return DKV_OK;
+}
+
+}  // namespace fwd
+
+bool tc_supported(int dtype, int head_dim, int heads, int kv_heads) {
+  if (dtype != DKV_BF16) return false;
+  if (head_dim != 64 && head_dim != 128) return false;
+  if (kv_heads <= 0 || heads % kv_heads) return false;
+  const int G = heads / kv_heads;
+  return G <= 128 && (128 % G) == 0;
+}
+
+int launch_tc_fwd(const SimtArgs& a, cudaStream_t st) {
+  if (a.head_dim == 128) return fwd::launch<128>(a, st);
+  return fwd::launch<64>(a, st);
+}
+
+}  // namespace dkv

@@ -1,0 +1,296 @@
+// simt_attn.cu -- fp32 SIMT DualKV kernels (any head_dim <= 256, any GQA ratio,
+// fp32 or bf16 storage).  These serve the fp32 dtype (BASELINE config C1) and
+// shapes the tcgen05 path does not take; compute is fp32 with exact expf.
+//
+// Semantics follow the reference tile core (fa2.py:112-229, kernel.py:177-305):
+// query row r of sequence i (logical position ctx_len + r) sees all context
+// keys and own keys 0..r; context gradients are summed over sequences in fp32
+// and cast once.
+#include "dkv_internal.h"
+
+namespace dkv {
+
+template <typename T>
+DKV_DEVICE float ldf(const T* p);
+template <>
+DKV_DEVICE float ldf<float>(const float* p) { return __ldg(p); }
+template <>
+DKV_DEVICE float ldf<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+
+template <typename T>
+DKV_DEVICE void stf(T* p, float v);
+template <>
+DKV_DEVICE void stf<float>(float* p, float v) { *p = v; }
+template <>
+DKV_DEVICE void stf<__nv_bfloat16>(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+DKV_DEVICE float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+constexpr int kMaxPerLane = 8;  // head_dim <= 256
+
+// binary search: sequence containing packed row t
+DKV_DEVICE int seq_of_row(const int32_t* cu, int n, int t) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (cu[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------- forward
+// one warp per (packed query row, head); lanes split head_dim
+template <typename T>
+__global__ void simt_fwd_kernel(SimtArgs a) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= a.total_q * a.heads) return;
+  const int t = gw / a.heads, h = gw % a.heads;
+  const int hk = h / (a.heads / a.kv_heads);
+  const int s = seq_of_row(a.cu, a.num_seqs, t);
+  const int r = t - a.cu[s];
+  const int seq0 = a.cu[s];
+  const int D = a.head_dim;
+  const T* q = static_cast<const T*>(a.q) + (static_cast<int64_t>(t) * a.heads + h) * D;
+  float qr[kMaxPerLane], acc[kMaxPerLane];
+#pragma unroll
+  for (int i = 0; i < kMaxPerLane; ++i) {
+    int e = lane + 32 * i;
+    qr[i] = e < D ? ldf(q + e) : 0.f;
+    acc[i] = 0.f;
+  }
+  float m = -INFINITY, l = 0.f;
+  auto visit = [&](const T* kbase, const T* vbase, int j) {
+    const T* kr = kbase + (static_cast<int64_t>(j) * a.kv_heads + hk) * D;
+    float part = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxPerLane; ++i) {
+      int e = lane + 32 * i;
+      if (e < D) part += qr[i] * ldf(kr + e);
+    }
+    float sc = warp_sum(part) * a.scale;
+    float mn = fmaxf(m, sc);
+    float alpha = expf(m - mn);  // m = -inf first time -> 0
+    float p = expf(sc - mn);
+    l = l * alpha + p;
+    const T* vr = vbase + (static_cast<int64_t>(j) * a.kv_heads + hk) * D;
+#pragma unroll
+    for (int i = 0; i < kMaxPerLane; ++i) {
+      int e = lane + 32 * i;
+      if (e < D) acc[i] = acc[i] * alpha + p * ldf(vr + e);
+    }
+    m = mn;
+  };
+  for (int j = 0; j < a.ctx_len; ++j) visit(static_cast<const T*>(a.k_ctx), static_cast<const T*>(a.v_ctx), j);
+  const T* kown = static_cast<const T*>(a.k) + static_cast<int64_t>(seq0) * a.kv_heads * D;
+  const T* vown = static_cast<const T*>(a.v) + static_cast<int64_t>(seq0) * a.kv_heads * D;
+  for (int j = 0; j <= r; ++j) visit(kown, vown, j);
+  T* o = static_cast<T*>(a.out) + (static_cast<int64_t>(t) * a.heads + h) * D;
+  const float inv = 1.f / l;
+#pragma unroll
+  for (int i = 0; i < kMaxPerLane; ++i) {
+    int e = lane + 32 * i;
+    if (e < D) stf(o + e, acc[i] * inv);
+  }
+  if (lane == 0) a.lse[static_cast<int64_t>(h) * a.total_q + t] = m + logf(l);
+}
+
+// ---------------------------------------------------------------- backward: dQ
+// D_row[h, t] = sum_d dO*O computed by the preprocess kernel (fa2.py:232-234)
+template <typename T>
+__global__ void simt_bwd_dq_kernel(SimtArgs a, const float* drow) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= a.total_q * a.heads) return;
+  const int t = gw / a.heads, h = gw % a.heads;
+  const int hk = h / (a.heads / a.kv_heads);
+  const int s = seq_of_row(a.cu, a.num_seqs, t);
+  const int r = t - a.cu[s];
+  const int seq0 = a.cu[s];
+  const int D = a.head_dim;
+  const int64_t qoff = (static_cast<int64_t>(t) * a.heads + h) * D;
+  float qr[kMaxPerLane], gr[kMaxPerLane], dq[kMaxPerLane];
+#pragma unroll
+  for (int i = 0; i < kMaxPerLane; ++i) {
+    int e = lane + 32 * i;
+    qr[i] = e < D ? ldf(static_cast<const T*>(a.q) + qoff + e) : 0.f;
+    gr[i] = e < D ? ldf(static_cast<const T*>(a.dout) + qoff + e) : 0.f;
+    dq[i] = 0.f;
+  }
+  const float lse = a.lse[static_cast<int64_t>(h) * a.total_q + t];
+  const float dr = drow[static_cast<int64_t>(h) * a.total_q + t];
+  auto visit = [&](const T* kbase, const T* vbase, int j) {
+    const int64_t ko = (static_cast<int64_t>(j) * a.kv_heads + hk) * D;
+    float sp = 0.f, dp = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxPerLane; ++i) {
+      int e = lane + 32 * i;
+      if (e < D) {
+        sp += qr[i] * ldf(kbase + ko + e);
+        dp += gr[i] * ldf(vbase + ko + e);
+      }
+    }
+    sp = warp_sum(sp);
+    dp = warp_sum(dp);
+    float p = expf(sp * a.scale - lse);
+    float ds = p * (dp - dr) * a.scale;
+#pragma unroll
+    for (int i = 0; i < kMaxPerLane; ++i) {
+      int e = lane + 32 * i;
+      if (e < D) dq[i] += ds * ldf(kbase + ko + e);
+    }
+  };
+  for (int j = 0; j < a.ctx_len; ++j) visit(static_cast<const T*>(a.k_ctx), static_cast<const T*>(a.v_ctx), j);
+  const T* kown = static_cast<const T*>(a.k) + static_cast<int64_t>(seq0) * a.kv_heads * D;
+  const T* vown = static_cast<const T*>(a.v) + static_cast<int64_t>(seq0) * a.kv_heads * D;
+  for (int j = 0; j <= r; ++j) visit(kown, vown, j);
+#pragma unroll
+  for (int i = 0; i < kMaxPerLane; ++i) {
+    int e = lane + 32 * i;
+    if (e < D) stf(static_cast<T*>(a.dq) + qoff + e, dq[i]);
+  }
+}
+
+// ---------------------------------------------------------------- backward: dK/dV
+// one warp per (key row, kv head).  Own-region key j of sequence s sums over
+// query rows r >= j of s and all G query heads of the group.  Context key j
+// sums over every query row of sequences [s_begin, s_end) (a "chunk"), in
+// sequence order, into fp32, then either casts once (ctx_out_*) or writes the
+// fp32 partial (instrumentation / deterministic fold).
+template <typename T>
+__global__ void simt_bwd_dkv_kernel(SimtArgs a, const float* drow, int own_rows, int chunk,
+                                    int num_chunks, float* ctx_part) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int D = a.head_dim;
+  const int G = a.heads / a.kv_heads;
+  const int64_t n_own = static_cast<int64_t>(own_rows) * a.kv_heads;
+  const int64_t n_ctx = static_cast<int64_t>(a.ctx_len) * a.kv_heads * num_chunks;
+  if (gw >= n_own + n_ctx) return;
+  const bool is_ctx = gw >= n_own;
+  int j, hk, s_lo, s_hi, chunk_id = 0;
+  const T *kb, *vb;
+  if (!is_ctx) {
+    const int t = gw / a.kv_heads;
+    hk = gw % a.kv_heads;
+    const int s = seq_of_row(a.cu, a.num_seqs, t);
+    j = t - a.cu[s];
+    s_lo = s;
+    s_hi = s + 1;
+    kb = static_cast<const T*>(a.k);
+    vb = static_cast<const T*>(a.v);
+  } else {
+    int64_t c = gw - n_own;
+    chunk_id = static_cast<int>(c / (static_cast<int64_t>(a.ctx_len) * a.kv_heads));
+    int rem = static_cast<int>(c % (static_cast<int64_t>(a.ctx_len) * a.kv_heads));
+    j = rem / a.kv_heads;
+    hk = rem % a.kv_heads;
+    s_lo = chunk_id * chunk;
+    s_hi = min(a.num_seqs, s_lo + chunk);
+    kb = static_cast<const T*>(a.k_ctx);
+    vb = static_cast<const T*>(a.v_ctx);
+  }
+  const int64_t krow = is_ctx ? j : (a.cu[s_lo] + j);
+  const int64_t ko = (krow * a.kv_heads + hk) * D;
+  float kr[kMaxPerLane], vr[kMaxPerLane], dk[kMaxPerLane], dv[kMaxPerLane];
+#pragma unroll
+  for (int i = 0; i < kMaxPerLane; ++i) {
+    int e = lane + 32 * i;
+    kr[i] = e < D ? ldf(kb + ko + e) : 0.f;
+    vr[i] = e < D ? ldf(vb + ko + e) : 0.f;
+    dk[i] = 0.f;
+    dv[i] = 0.f;
+  }
+  for (int s = s_lo; s < s_hi; ++s) {
+    const int r0 = a.cu[s], r1 = a.cu[s + 1];
+    const int first = is_ctx ? r0 : r0 + j;
+    for (int t = first; t < r1; ++t) {
+      for (int g = 0; g < G; ++g) {
+        const int h = hk * G + g;
+        const int64_t qo = (static_cast<int64_t>(t) * a.heads + h) * D;
+        float sp = 0.f, dp = 0.f;
+        float qv[kMaxPerLane], gv[kMaxPerLane];
+#pragma unroll
+        for (int i = 0; i < kMaxPerLane; ++i) {
+          int e = lane + 32 * i;
+          qv[i] = e < D ? ldf(static_cast<const T*>(a.q) + qo + e) : 0.f;
+          gv[i] = e < D ? ldf(static_cast<const T*>(a.dout) + qo + e) : 0.f;
+          sp += qv[i] * kr[i];
+          dp += gv[i] * vr[i];
+        }
+        sp = warp_sum(sp);
+        dp = warp_sum(dp);
+        const float p = expf(sp * a.scale - a.lse[static_cast<int64_t>(h) * a.total_q + t]);
+        const float ds = p * (dp - drow[static_cast<int64_t>(h) * a.total_q + t]) * a.scale;
+#pragma unroll
+        for (int i = 0; i < kMaxPerLane; ++i) {
+          dv[i] += p * gv[i];
+          dk[i] += ds * qv[i];
+        }
+      }
+    }
+  }
+  if (!is_ctx) {
+#pragma unroll
+    for (int i = 0; i < kMaxPerLane; ++i) {
+      int e = lane + 32 * i;
+      if (e < D) {
+        stf(static_cast<T*>(a.dk) + ko + e, dk[i]);
+        stf(static_cast<T*>(a.dv) + ko + e, dv[i]);
+      }
+    }
+  } else {
+    // fp32 partial for this chunk: [chunk][2][P][Hk][D]
+    const int64_t plane = static_cast<int64_t>(a.ctx_len) * a.kv_heads * D;
+    float* pk = ctx_part + static_cast<int64_t>(chunk_id) * 2 * plane + ko;
+    float* pv = pk + plane;
+#pragma unroll
+    for (int i = 0; i < kMaxPerLane; ++i) {
+      int e = lane + 32 * i;
+      if (e < D) {
+        pk[e] = dk[i];
+        pv[e] = dv[i];
+      }
+    }
+  }
+}
+
+void launch_simt_fwd(const SimtArgs& a, cudaStream_t st) {
+  const int64_t warps = a.total_q * a.heads;
+  if (warps == 0) return;
+  const int threads = 256;
+  const int64_t blocks = (warps * 32 + threads - 1) / threads;
+  if (a.dtype == DKV_F32)
+    simt_fwd_kernel<float><<<blocks, threads, 0, st>>>(a);
+  else
+    simt_fwd_kernel<__nv_bfloat16><<<blocks, threads, 0, st>>>(a);
+}
+
+void launch_simt_bwd(const SimtArgs& a, const float* drow, int chunk, int num_chunks, float* ctx_part,
+                     cudaStream_t st) {
+  const int threads = 256;
+  const int64_t w1 = a.total_q * a.heads;
+  if (w1 > 0) {
+    const int64_t b1 = (w1 * 32 + threads - 1) / threads;
+    if (a.dtype == DKV_F32)
+      simt_bwd_dq_kernel<float><<<b1, threads, 0, st>>>(a, drow);
+    else
+      simt_bwd_dq_kernel<__nv_bfloat16><<<b1, threads, 0, st>>>(a, drow);
+  }
+  const int64_t w2 = a.total_q * a.kv_heads + a.ctx_len * a.kv_heads * num_chunks;
+  if (w2 > 0) {
+    const int64_t b2 = (w2 * 32 + threads - 1) / threads;
+    if (a.dtype == DKV_F32)
+      simt_bwd_dkv_kernel<float><<<b2, threads, 0, st>>>(a, drow, static_cast<int>(a.total_q), chunk,
+                                                         num_chunks, ctx_part);
+    else
+      simt_bwd_dkv_kernel<__nv_bfloat16><<<b2, threads, 0, st>>>(a, drow, static_cast<int>(a.total_q),
+                                                                 chunk, num_chunks, ctx_part);
+  }
+}
+
+}  // namespace dkv

@@ -1,0 +1,46 @@
+// tma_host.h -- host-side TMA tensor-map encoding through the driver entry
+// point (no link-time dependency on libcuda).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+namespace dkv {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 3-D bf16 map over a row-major [rows, heads, dim] tensor: dims (dim, heads, rows),
+// box (64, box_heads, box_rows), SWIZZLE_128B (64 bf16 = 128 B inner box).
+inline bool make_map_3d_bf16(CUtensorMap* m, const void* base, int64_t rows, int64_t heads, int64_t dim,
+                             uint32_t box_heads, uint32_t box_rows) {
+  std::memset(m, 0, sizeof(*m));
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn || rows <= 0) return false;
+  cuuint64_t gdim[3] = {static_cast<cuuint64_t>(dim), static_cast<cuuint64_t>(heads),
+                        static_cast<cuuint64_t>(rows)};
+  cuuint64_t gstride[2] = {static_cast<cuuint64_t>(dim * 2), static_cast<cuuint64_t>(heads * dim * 2)};
+  cuuint32_t box[3] = {64u, box_heads, box_rows};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), gdim, gstride, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace dkv
