@@ -122,6 +122,15 @@ DKV_API int32_t dkv_segment_sum_rows(const void* src, void* dst, int32_t dtype, 
                              const int64_t* seg, const int64_t* src_idx, int64_t n_rows,
                              void* stream);
 
+/* Kernel timing for the bench harness: while enabled, the library records a
+ * CUDA event pair (on the launching stream) around every main attention
+ * kernel and counts every kernel it launches.  dkv_profile_end synchronises
+ * on the recorded events and returns the summed device milliseconds and
+ * launch counts of the forward and backward main kernels, plus all launches. */
+DKV_API int32_t dkv_profile_begin(void);
+DKV_API int32_t dkv_profile_end(double* fwd_ms, int32_t* fwd_launches, double* bwd_ms,
+                                int32_t* bwd_launches, int32_t* all_launches);
+
 /* Self-test of the UMMA operand layouts used by the kernels (debug aid):
  * 128x128 (or 128xN) bf16 product through TMA + tcgen05, D fp32 [128][N]. */
 DKV_API int32_t dkv_selftest_umma(int32_t mode, const void* a, const void* b, float* d, void* stream);

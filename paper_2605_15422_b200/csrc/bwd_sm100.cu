@@ -1,9 +1,477 @@
-// bwd_sm100.cu -- tcgen05 backward (placeholder until the kernel lands).
+// bwd_sm100.cu -- tcgen05/TMEM/TMA backward for DualKV attention (path 3 and
+// the backward of paths 1 / the replicated baseline).
+//
+// KV-stationary (SURVEY §7.4 design (C)): a CTA owns one 128-key tile of one
+// KV head and sweeps the 64-row query tiles that see it, accumulating dK and
+// dV in TMEM for ALL G query heads of the group at once (GQA packed into the
+// query tile rows, so the reference's per-tile GQA fold, fa2.py:224-227, is
+// free).  Work items:
+//   * own-region tiles (sequence s, key tile j): query tiles of s from the
+//     causal diagonal on; dK_d / dV_d are written once as bf16 (no merge);
+//   * shared-prompt tiles (chunk c of sequences, context tile j): all query
+//     tiles of the chunk's sequences (no causal mask); the fp32 dK_c / dV_c
+//     tile is reduce-added into one fp32 scratch (atomic mode) or stored as
+//     the chunk's partial (deterministic mode) -- then folded and cast once
+//     (kernel.py:279-285, Alg. 1/2).
+// dQ is accumulated across key tiles with fp32 red.global.add into dq_acc.
+//
+// Per query tile (B_q = 64 rows, B_k = 128 keys, d = 128):
+//   S^T  = K Q^T      (M128 N64  K128)  -> TMEM [0,64)
+//   dP^T = V dO^T     (M128 N64  K128)  -> TMEM [64,128)
+//   P^T = exp2(S^T*scale*log2e - lse2), dS^T = P^T (dP^T - D) * scale   (compute WG)
+//   dV  += P^T dO     (M128 N128 K64)   A = P^T (smem)   -> TMEM [256,384)
+//   dK  += dS^T Q     (M128 N128 K64)   A = dS^T (smem)  -> TMEM [384,512)
+//   dQ^T = K^T dS^T   (M128 N64  K128)  double-buffered  -> TMEM [128,256)
+// Roles: warps 0-3 compute (thread = key row), 4-7 dQ drain (thread = head-dim
+// lane) + dV epilogue, 8 TMA producer + TMEM allocator, 9 MMA issuer.
 #include "dkv_internal.h"
+#include "tma_host.h"
+
 namespace dkv {
-bool tc_bwd_supported(int, int, int, int) { return false; }
-int launch_tc_bwd(const SimtArgs&, float*, const float2*, float*, int, int, bool, cudaStream_t) {
-  set_error("tcgen05 backward not built");
-  return DKV_ERR_UNSUPPORTED;
+namespace bwd {
+
+constexpr int kBK = 128;  // keys per tile (MMA M)
+constexpr int kBQ = 64;   // query rows per tile (MMA N for S^T / dP^T / dQ^T)
+constexpr int D = 128;
+constexpr int kThreads = 320;
+constexpr int kStages = 3;
+constexpr int kKVBytes = kBK * D * 2;       // 32 KB
+constexpr int kKVPanel = kBK * 128;         // 16 KB
+constexpr int kQBytes = kBQ * D * 2;        // 16 KB
+constexpr int kQPanel = kBQ * 128;          // 8 KB
+constexpr int kPBytes = kBK * kBQ * 2;      // 16 KB
+constexpr int kOffK = 0;
+constexpr int kOffV = kOffK + kKVBytes;
+constexpr int kOffQ = kOffV + kKVBytes;
+constexpr int kOffDO = kOffQ + kStages * kQBytes;
+constexpr int kOffP = kOffDO + kStages * kQBytes;
+constexpr int kOffDS = kOffP + kPBytes;
+constexpr int kOffLD = kOffDS + kPBytes;
+constexpr int kOffBar = kOffLD + kStages * kBQ * 8;
+constexpr int kSmemBytes = kOffBar + 512 + 1024;
+
+struct Params {
+  CUtensorMap tm_q, tm_do, tm_k, tm_v, tm_kc, tm_vc;
+  const float2* dpack;  // [Hk][T][G] (lse*log2e, D)
+  float* dq_acc;        // [T][H][D] f32
+  __nv_bfloat16* dk;    // [T][Hk][D]
+  __nv_bfloat16* dv;
+  float* ctx_acc;       // [parts][2][P][Hk][D]
+  const int32_t* cu;
+  int num_seqs, total_q, ctx_len, heads, kv_heads, group, tq;
+  int chunk, n_ctx_items, n_ctx_tiles;
+  int atomic_ctx;
+  float scale, scale_log2;
+};
+
+struct Bars {
+  uint64_t kv_full, sdp_full, sdp_empty, pds_full, pds_empty, kv_done;
+  uint64_t q_full[kStages], q_empty[kStages];
+  uint64_t dq_full[2], dq_empty[2];
+  uint32_t tmem_base;
+};
+
+// The query tiles of one work item, walked identically by every role.
+struct QIter {
+  const int32_t* cu;
+  int tq, s, s_end, tok, rlen;
+  __device__ void begin(const int32_t* cu_, int tq_, int s0, int s1, int tok0) {
+    cu = cu_;
+    tq = tq_;
+    s = s0;
+    s_end = s1;
+    tok = tok0;
+    rlen = cu[s + 1] - cu[s];
+    skip_empty();
+  }
+  __device__ void skip_empty() {
+    while (s < s_end && tok >= rlen) {
+      ++s;
+      tok = 0;
+      if (s < s_end) rlen = cu[s + 1] - cu[s];
+    }
+  }
+  __device__ bool valid() const { return s < s_end; }
+  __device__ void next() {
+    tok += tq;
+    skip_empty();
+  }
+};
+
+__device__ __forceinline__ void red_add(float* p, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Bars& bar = *reinterpret_cast<Bars*>(base + kOffBar);
+  float2* sLD = reinterpret_cast<float2*>(base + kOffLD);
+
+  // ---- decode the work item
+  const int bid = blockIdx.x;
+  bool is_ctx;
+  int hk, ktile, s0, s1, tok_first, kv_len, kv_row0;
+  if (bid < p.n_ctx_items) {
+    is_ctx = true;
+    const int per_chunk = p.n_ctx_tiles * p.kv_heads;
+    const int chunk_id = bid / per_chunk;
+    const int rem = bid % per_chunk;
+    ktile = rem / p.kv_heads;
+    hk = rem % p.kv_heads;
+    s0 = chunk_id * p.chunk;
+    s1 = min(p.num_seqs, s0 + p.chunk);
+    tok_first = 0;
+    kv_len = p.ctx_len;
+    kv_row0 = 0;
+  } else {
+    is_ctx = false;
+    const int b2 = bid - p.n_ctx_items;
+    hk = b2 % p.kv_heads;
+    const int r2 = b2 / p.kv_heads;
+    s0 = r2 % p.num_seqs;
+    ktile = r2 / p.num_seqs;
+    s1 = s0 + 1;
+    kv_len = p.cu[s0 + 1] - p.cu[s0];
+    if (ktile * kBK >= kv_len) return;
+    tok_first = (ktile * kBK / p.tq) * p.tq;
+    kv_row0 = p.cu[s0];
+  }
+  const int kbase = ktile * kBK;  // region-local first key of the tile
+  int nq = 0;
+  {
+    QIter it;
+    it.begin(p.cu, p.tq, s0, s1, tok_first);
+    for (; it.valid(); it.next()) ++nq;
+  }
+  if (nq == 0) return;  // context chunk of empty responses: scratch already zero
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar.kv_full, 1);
+    mbar_init(&bar.sdp_full, 1);
+    mbar_init(&bar.sdp_empty, 128);
+    mbar_init(&bar.pds_full, 128);
+    mbar_init(&bar.pds_empty, 1);
+    mbar_init(&bar.kv_done, 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&bar.q_full[i], 1 + 32);
+      mbar_init(&bar.q_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar.dq_full[i], 1);
+      mbar_init(&bar.dq_empty[i], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 8) tmem_alloc<512>(&bar.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bar.tmem_base;
+  const int G = p.group;
+
+  if (warp == 8) {
+    // ================= producer: K/V once, then (Q, dO, lse/D) per query tile
+    const CUtensorMap* mk = is_ctx ? &p.tm_kc : &p.tm_k;
+    const CUtensorMap* mv = is_ctx ? &p.tm_vc : &p.tm_v;
+    if (lane == 0) {
+      tma_prefetch(&p.tm_q);
+      tma_prefetch(&p.tm_do);
+      tma_prefetch(mk);
+      tma_prefetch(mv);
+      mbar_arrive_expect_tx(&bar.kv_full, 2 * kKVBytes);
+      for (int pn = 0; pn < 2; ++pn) {
+        tma_load_3d(base + kOffK + pn * kKVPanel, mk, &bar.kv_full, pn * 64, hk, kv_row0 + kbase);
+        tma_load_3d(base + kOffV + pn * kKVPanel, mv, &bar.kv_full, pn * 64, hk, kv_row0 + kbase);
+      }
+    }
+    const uint64_t pol_q = policy_evict_last();
+    QIter it;
+    it.begin(p.cu, p.tq, s0, s1, tok_first);
+    for (int i = 0; it.valid(); it.next(), ++i) {
+      const int st = i % kStages;
+      const uint32_t ph = (i / kStages) & 1;
+      mbar_wait(&bar.q_empty[st], ph ^ 1);
+      const int row0 = p.cu[it.s] + it.tok;
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&bar.q_full[st], 2 * kQBytes);
+        for (int pn = 0; pn < 2; ++pn) {
+          tma_load_3d_hint(base + kOffQ + st * kQBytes + pn * kQPanel, &p.tm_q, &bar.q_full[st], pn * 64,
+                           hk * G, row0, pol_q);
+          tma_load_3d_hint(base + kOffDO + st * kQBytes + pn * kQPanel, &p.tm_do, &bar.q_full[st], pn * 64,
+                           hk * G, row0, pol_q);
+        }
+      }
+      // (lse*log2e, D) of the 64 rows, rows beyond the sequence end -> (+inf, 0)
+      for (int c = lane; c < kBQ; c += 32) {
+        const int tok = it.tok + c / G;
+        float2 v = make_float2(INFINITY, 0.f);
+        if (tok < it.rlen) v = p.dpack[(static_cast<int64_t>(hk) * p.total_q + p.cu[it.s] + tok) * G + c % G];
+        sLD[st * kBQ + c] = v;
+      }
+      mbar_arrive(&bar.q_full[st]);
+    }
+  } else if (warp == 9) {
+    // ================= MMA issuer
+    if (elect_one()) {
+      const uint32_t tS = tmem, tdP = tmem + 64, tdQ = tmem + 128, tdV = tmem + 256, tdK = tmem + 384;
+      const uint32_t id_sdp = idesc_bf16_f32(kBK, kBQ, false, false);
+      const uint32_t id_kv = idesc_bf16_f32(kBK, D, false, true);
+      const uint32_t id_dq = idesc_bf16_f32(D, kBQ, true, true);
+      const uint32_t aK = smem_u32(base + kOffK), aV = smem_u32(base + kOffV);
+      const uint32_t aP = smem_u32(base + kOffP), aDS = smem_u32(base + kOffDS);
+      mbar_wait(&bar.kv_full, 0);
+      for (int i = 0; i <= nq; ++i) {
+        if (i < nq) {
+          const int st = i % kStages;
+          mbar_wait(&bar.q_full[st], (i / kStages) & 1);
+          if (i > 0) mbar_wait(&bar.sdp_empty, (i - 1) & 1);
+          tc_fence_after();
+          const uint32_t aQ = smem_u32(base + kOffQ + st * kQBytes);
+          const uint32_t aDO = smem_u32(base + kOffDO + st * kQBytes);
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t oa = (k >> 2) * kKVPanel + (k & 3) * 32;
+            const uint32_t ob = (k >> 2) * kQPanel + (k & 3) * 32;
+            mma_ss(tS, sdesc_sw128(aK + oa, 16, 1024), sdesc_sw128(aQ + ob, 16, 1024), id_sdp, k > 0);
+          }
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t oa = (k >> 2) * kKVPanel + (k & 3) * 32;
+            const uint32_t ob = (k >> 2) * kQPanel + (k & 3) * 32;
+            mma_ss(tdP, sdesc_sw128(aV + oa, 16, 1024), sdesc_sw128(aDO + ob, 16, 1024), id_sdp, k > 0);
+          }
+          mma_commit(&bar.sdp_full);
+        }
+        if (i > 0) {
+          const int j = i - 1;
+          const int sj = j % kStages;
+          const uint32_t aQ = smem_u32(base + kOffQ + sj * kQBytes);
+          const uint32_t aDO = smem_u32(base + kOffDO + sj * kQBytes);
+          mbar_wait(&bar.pds_full, j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < kBQ / 16; ++k)
+            mma_ss(tdV, sdesc_sw128(aP + k * 32, 16, 1024), sdesc_sw128(aDO + k * 2048, kQPanel, 1024), id_kv,
+                   (j > 0 || k > 0) ? 1u : 0u);
+#pragma unroll
+          for (int k = 0; k < kBQ / 16; ++k)
+            mma_ss(tdK, sdesc_sw128(aDS + k * 32, 16, 1024), sdesc_sw128(aQ + k * 2048, kQPanel, 1024), id_kv,
+                   (j > 0 || k > 0) ? 1u : 0u);
+          mma_commit(&bar.q_empty[sj]);
+          const int b = j & 1;
+          mbar_wait(&bar.dq_empty[b], ((j >> 1) & 1) ^ 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            mma_ss(tdQ + b * 64, sdesc_sw128(aK + k * 2048, kKVPanel, 1024), sdesc_sw128(aDS + k * 2048, kPBytes, 1024),
+                   id_dq, k > 0);
+          mma_commit(&bar.dq_full[b]);
+          mma_commit(&bar.pds_empty);
+        }
+      }
+      mma_commit(&bar.kv_done);
+    }
+  } else if (warp < 4) {
+    // ================= compute WG: thread = key row r of the tile
+    const int r = warp * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const int key = kbase + r;  // region-local key index
+    uint8_t* sP = base + kOffP;
+    uint8_t* sDS = base + kOffDS;
+    QIter it;
+    it.begin(p.cu, p.tq, s0, s1, tok_first);
+    for (int i = 0; it.valid(); it.next(), ++i) {
+      const int st = i % kStages;
+      mbar_wait(&bar.q_full[st], (i / kStages) & 1);
+      mbar_wait(&bar.sdp_full, i & 1);
+      tc_fence_after();
+      uint32_t us[64], ud[64];
+      tmem_ld32(tmem + lane_off + 0, *reinterpret_cast<uint32_t(*)[32]>(&us[0]));
+      tmem_ld32(tmem + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(&us[32]));
+      tmem_ld32(tmem + lane_off + 64, *reinterpret_cast<uint32_t(*)[32]>(&ud[0]));
+      tmem_ld32(tmem + lane_off + 96, *reinterpret_cast<uint32_t(*)[32]>(&ud[32]));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bar.sdp_empty);
+      const float2* ld = sLD + st * kBQ;
+      // key visible to query column c?
+      //   context tile: key < P (all query rows of the chunk see the whole prompt)
+      //   own tile:     key <= query token (causal; implies key < R_s for valid rows)
+      const bool key_ok = is_ctx ? key < kv_len : true;
+      uint32_t pp[32], pd[32];
+#pragma unroll
+      for (int c2 = 0; c2 < 32; ++c2) {
+        float pv[2], dv2[2];
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c = 2 * c2 + h2;
+          const float2 lsd = ld[c];
+          const int qtok = it.tok + c / G;
+          const bool vis = key_ok && (is_ctx || key <= qtok);
+          const float e = ex2(fmaf(__uint_as_float(us[c]), p.scale_log2, -lsd.x));
+          const float pr = vis ? e : 0.f;
+          pv[h2] = pr;
+          dv2[h2] = pr * (__uint_as_float(ud[c]) - lsd.y) * p.scale;
+        }
+        pp[c2] = pack_bf16(pv[0], pv[1]);
+        pd[c2] = pack_bf16(dv2[0], dv2[1]);
+      }
+      mbar_wait(&bar.pds_empty, (i & 1) ^ 1);
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        const uint32_t off = sw128_offset(r, ch);
+        *reinterpret_cast<uint4*>(sP + off) = make_uint4(pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]);
+        *reinterpret_cast<uint4*>(sDS + off) = make_uint4(pd[4 * ch], pd[4 * ch + 1], pd[4 * ch + 2], pd[4 * ch + 3]);
+      }
+      fence_async_smem();
+      mbar_arrive(&bar.pds_full);
+    }
+  } else {
+    // ================= dQ drain WG: thread = head-dim lane d
+    const int d = (warp - 4) * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>((warp - 4) * 32) << 16;
+    QIter it;
+    it.begin(p.cu, p.tq, s0, s1, tok_first);
+    for (int i = 0; it.valid(); it.next(), ++i) {
+      const int b = i & 1;
+      mbar_wait(&bar.dq_full[b], (i >> 1) & 1);
+      tc_fence_after();
+      uint32_t u[64];
+      tmem_ld32(tmem + lane_off + 128 + b * 64, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
+      tmem_ld32(tmem + lane_off + 128 + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bar.dq_empty[b]);
+      const int64_t row_tok0 = p.cu[it.s] + it.tok;
+#pragma unroll
+      for (int c = 0; c < kBQ; ++c) {
+        const int tl = c / G;
+        if (it.tok + tl < it.rlen)
+          red_add(p.dq_acc + ((row_tok0 + tl) * p.heads + hk * G + c % G) * D + d, __uint_as_float(u[c]));
+      }
+    }
+  }
+
+  // ================= dK / dV epilogue: warps 0-3 dK, warps 4-7 dV (thread = key row)
+  if (warp < 8) {
+    const bool do_k = warp < 4;
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tcol = tmem + lane_off + (do_k ? 384 : 256);
+    mbar_wait(&bar.kv_done, 0);
+    tc_fence_after();
+    const int key = kbase + r;
+    const bool ok = key < kv_len;
+#pragma unroll 1
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      uint32_t u[32];
+      tmem_ld32(tcol + c0, u);
+      tmem_wait_ld();
+      if (!ok) continue;
+      if (is_ctx) {
+        const int64_t plane = static_cast<int64_t>(p.ctx_len) * p.kv_heads * D;
+        const int chunk_id = s0 / p.chunk;
+        float* dst = p.ctx_acc + (p.atomic_ctx ? 0 : static_cast<int64_t>(chunk_id) * 2 * plane) +
+                     (do_k ? 0 : plane) + (static_cast<int64_t>(key) * p.kv_heads + hk) * D + c0;
+        if (p.atomic_ctx) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            red_add_v4(dst + i, __uint_as_float(u[i]), __uint_as_float(u[i + 1]), __uint_as_float(u[i + 2]),
+                       __uint_as_float(u[i + 3]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(dst + i) = make_float4(__uint_as_float(u[i]), __uint_as_float(u[i + 1]),
+                                                              __uint_as_float(u[i + 2]), __uint_as_float(u[i + 3]));
+        }
+      } else {
+        __nv_bfloat16* dst = (do_k ? p.dk : p.dv) + ((static_cast<int64_t>(kv_row0) + key) * p.kv_heads + hk) * D + c0;
+        uint4 v[4];
+        uint32_t* w = reinterpret_cast<uint32_t*>(v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) w[i] = pack_bf16(__uint_as_float(u[2 * i]), __uint_as_float(u[2 * i + 1]));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) reinterpret_cast<uint4*>(dst)[i] = v[i];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace bwd
+
+bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads) {
+  if (dtype != DKV_BF16 || head_dim != bwd::D) return false;
+  if (kv_heads <= 0 || heads % kv_heads) return false;
+  const int G = heads / kv_heads;
+  return G <= bwd::kBQ && (bwd::kBQ % G) == 0;
+}
+
+int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const float2* dpack, float* ctx_acc, int chunk, int num_chunks,
+                  bool atomic_ctx, cudaStream_t st) {
+  using namespace bwd;
+  Params p{};
+  const int G = a.heads / a.kv_heads;
+  const int tq = kBQ / G;
+  if (!make_map_3d_bf16(&p.tm_q, a.q, a.total_q, a.heads, D, G, tq) ||
+      !make_map_3d_bf16(&p.tm_do, a.dout, a.total_q, a.heads, D, G, tq) ||
+      !make_map_3d_bf16(&p.tm_k, a.k, a.total_q, a.kv_heads, D, 1, kBK) ||
+      !make_map_3d_bf16(&p.tm_v, a.v, a.total_q, a.kv_heads, D, 1, kBK)) {
+    set_error("cuTensorMapEncodeTiled failed (backward q/dO/k/v)");
+    return DKV_ERR_CUDA;
+  }
+  if (a.ctx_len > 0) {
+    if (!make_map_3d_bf16(&p.tm_kc, a.k_ctx, a.ctx_len, a.kv_heads, D, 1, kBK) ||
+        !make_map_3d_bf16(&p.tm_vc, a.v_ctx, a.ctx_len, a.kv_heads, D, 1, kBK)) {
+      set_error("cuTensorMapEncodeTiled failed (backward k_ctx/v_ctx)");
+      return DKV_ERR_CUDA;
+    }
+  }
+  p.dpack = dpack;
+  p.dq_acc = dq_acc;
+  p.dk = static_cast<__nv_bfloat16*>(a.dk);
+  p.dv = static_cast<__nv_bfloat16*>(a.dv);
+  p.ctx_acc = ctx_acc;
+  p.cu = a.cu;
+  p.num_seqs = a.num_seqs;
+  p.total_q = a.total_q;
+  p.ctx_len = a.ctx_len;
+  p.heads = a.heads;
+  p.kv_heads = a.kv_heads;
+  p.group = G;
+  p.tq = tq;
+  p.chunk = chunk;
+  p.n_ctx_tiles = (a.ctx_len + kBK - 1) / kBK;
+  p.n_ctx_items = p.n_ctx_tiles * a.kv_heads * num_chunks;
+  p.atomic_ctx = atomic_ctx ? 1 : 0;
+  p.scale = a.scale;
+  p.scale_log2 = a.scale * 1.4426950408889634f;
+  const int max_tiles = (a.max_seqlen + kBK - 1) / kBK;
+  const int64_t grid = static_cast<int64_t>(p.n_ctx_items) + static_cast<int64_t>(max_tiles) * a.num_seqs * a.kv_heads;
+  if (grid == 0) return DKV_OK;
+  if (grid > 0x7fffffff) {
+    set_error("backward grid too large");
+    return DKV_ERR_UNSUPPORTED;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dualkv_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    attr = true;
+  }
+  dualkv_bwd_kernel<<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(p);
+  return DKV_OK;
+}
+
 }  // namespace dkv

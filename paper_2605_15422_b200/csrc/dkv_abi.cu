@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "dkv_internal.h"
 
@@ -15,6 +16,32 @@ namespace dkv {
 
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+
+// ---- profiling hooks (bench harness only; off by default)
+struct ProfState {
+  bool on = false;
+  int launches = 0;
+  std::vector<std::pair<int, cudaEvent_t>> ev;  // (kind*2 + is_end, event)
+};
+static ProfState g_prof;
+
+void prof_main_begin(int kind, cudaStream_t st) {
+  if (!g_prof.on) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  g_prof.ev.push_back({kind * 2, e});
+}
+void prof_main_end(int kind, cudaStream_t st) {
+  if (!g_prof.on) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  g_prof.ev.push_back({kind * 2 + 1, e});
+}
+void prof_count(int launches) {
+  if (g_prof.on) g_prof.launches += launches;
+}
 
 static int fail(int code, const std::string& msg) {
   set_error(msg);
@@ -84,12 +111,15 @@ static int fwd_impl(const dkv_fwd_params* p, bool dualkv, void* stream, const ch
   a.lse = p->lse;
   auto st = static_cast<cudaStream_t>(stream);
   if (a.total_q == 0) return DKV_OK;
+  prof_main_begin(0, st);
   if (tc_supported(a.dtype, a.head_dim, a.heads, a.kv_heads)) {
     rc = launch_tc_fwd(a, st);
     if (rc) return rc;
   } else {
     launch_simt_fwd(a, st);
   }
+  prof_main_end(0, st);
+  prof_count(1);
   return check_launch(fn);
 }
 
@@ -174,16 +204,26 @@ static int bwd_impl(const dkv_bwd_params* p, void* ws, size_t ws_bytes, bool dua
     float* dq_acc = reinterpret_cast<float*>(w + L.dq_acc);
     cudaMemsetAsync(dq_acc, 0, static_cast<size_t>(a.total_q) * a.heads * a.head_dim * 4, st);
     const bool atomic_ctx = L.num_parts == 1 && L.num_chunks > 1;
-    if (plane > 0 && atomic_ctx) cudaMemsetAsync(ctx, 0, 2 * plane * 4, st);
+    // chunks whose responses are all empty write nothing: start from zero
+    if (plane > 0) cudaMemsetAsync(ctx, 0, static_cast<size_t>(L.num_parts) * 2 * plane * 4, st);
     launch_rowsum_do_o(a, nullptr, dpack, st);
+    prof_main_begin(1, st);
     rc = launch_tc_bwd(a, dq_acc, reinterpret_cast<const float2*>(dpack), ctx, L.chunk, L.num_chunks, atomic_ctx, st);
     if (rc) return rc;
+    prof_main_end(1, st);
     launch_convert(dq_acc, p->dq, a.dtype, static_cast<int64_t>(a.total_q) * a.heads * a.head_dim, st);
+    prof_count(3);
   } else {
     launch_rowsum_do_o(a, drow, nullptr, st);
+    prof_main_begin(1, st);
     launch_simt_bwd(a, drow, L.chunk, L.num_chunks, ctx, st);
+    prof_main_end(1, st);
+    prof_count(3);
   }
-  if (plane > 0) launch_fold_convert(ctx, L.num_parts, plane, p->dk_ctx, p->dv_ctx, a.dtype, st);
+  if (plane > 0) {
+    launch_fold_convert(ctx, L.num_parts, plane, p->dk_ctx, p->dv_ctx, a.dtype, st);
+    prof_count(1);
+  }
   return check_launch(fn);
 }
 
@@ -194,6 +234,43 @@ using namespace dkv;
 extern "C" {
 
 int32_t dkv_abi_version(void) { return DKV_ABI_VERSION; }
+
+int32_t dkv_profile_begin(void) {
+  for (auto& e : g_prof.ev) cudaEventDestroy(e.second);
+  g_prof.ev.clear();
+  g_prof.launches = 0;
+  g_prof.on = true;
+  return DKV_OK;
+}
+
+int32_t dkv_profile_end(double* fwd_ms, int32_t* fwd_launches, double* bwd_ms, int32_t* bwd_launches,
+                        int32_t* all_launches) {
+  g_prof.on = false;
+  double ms[2] = {0, 0};
+  int cnt[2] = {0, 0};
+  cudaEvent_t open[2] = {nullptr, nullptr};
+  for (auto& e : g_prof.ev) {
+    const int kind = e.first / 2;
+    if ((e.first & 1) == 0) {
+      open[kind] = e.second;
+    } else if (open[kind]) {
+      cudaEventSynchronize(e.second);
+      float t = 0.f;
+      cudaEventElapsedTime(&t, open[kind], e.second);
+      ms[kind] += t;
+      cnt[kind] += 1;
+      open[kind] = nullptr;
+    }
+  }
+  for (auto& e : g_prof.ev) cudaEventDestroy(e.second);
+  g_prof.ev.clear();
+  if (fwd_ms) *fwd_ms = ms[0];
+  if (fwd_launches) *fwd_launches = cnt[0];
+  if (bwd_ms) *bwd_ms = ms[1];
+  if (bwd_launches) *bwd_launches = cnt[1];
+  if (all_launches) *all_launches = g_prof.launches;
+  return check_launch("dkv_profile_end");
+}
 const char* dkv_last_error(void) { return g_err.c_str(); }
 int32_t dkv_uses_tensor_cores(int32_t dtype, int64_t head_dim, int64_t heads, int64_t kv_heads) {
   return tc_supported(dtype, static_cast<int>(head_dim), static_cast<int>(heads), static_cast<int>(kv_heads)) ? 1

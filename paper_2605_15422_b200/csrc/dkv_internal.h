@@ -35,6 +35,11 @@ struct SimtArgs {
 
 void set_error(const std::string& msg);
 
+// profiling hooks (dkv_abi.cu): kind 0 = forward main kernel, 1 = backward main kernel
+void prof_main_begin(int kind, cudaStream_t st);
+void prof_main_end(int kind, cudaStream_t st);
+void prof_count(int launches);
+
 // simt_attn.cu
 void launch_simt_fwd(const SimtArgs& a, cudaStream_t st);
 void launch_simt_bwd(const SimtArgs& a, const float* drow, int chunk, int num_chunks, float* ctx_part,
