@@ -104,7 +104,7 @@ def test_fp32_vs_f64_oracle(case, cuda_device):
         assert_close_abs(to_np(got), ref, F32_ATOL * max(1.0, np.abs(ref).max()), name)
 
 
-@pytest.mark.parametrize("name", [n for n in golden_names("dualkv") if "f64" not in n])
+@pytest.mark.parametrize("name", [n for n in golden_names("dualkv") if load_golden(n)[0]["prec"] != "f64"])
 def test_golden_vectors(name, cuda_device):
     """GPU vs the reference's own outputs stored in tests/golden (f32 / bf16 cases)."""
     import paper_2605_15422_b200 as dkv
