@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
 }  // namespace bwd
 
 bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads) {
-  if (dtype != DKV_BF16 || head_dim != bwd::D) return false;
+  if (dtype != DKV_BF16 || head_dim != bwd::D || force_simt()) return false;
   if (kv_heads <= 0 || heads % kv_heads) return false;
   const int G = heads / kv_heads;
   return G <= bwd::kBQ && (bwd::kBQ % G) == 0;

@@ -52,6 +52,7 @@ void launch_fold_convert(const float* partials, int num_parts, int64_t plane, vo
 void launch_convert(const float* src, void* dst, int dtype, int64_t n, cudaStream_t st);
 
 // sm100 tensor-core paths (fwd_sm100.cu / bwd_sm100.cu)
+bool force_simt();  // DKV_FORCE_SIMT=1: route everything to the SIMT kernels (cross-checks)
 bool tc_supported(int dtype, int head_dim, int heads, int kv_heads);
 bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads);
 int launch_tc_fwd(const SimtArgs& a, cudaStream_t st);

@@ -25,6 +25,8 @@
 #include "dkv_internal.h"
 #include "tma_host.h"
 
+#include <cstdlib>
+
 namespace dkv {
 namespace fwd {
 
@@ -374,8 +376,16 @@ int launch(const SimtArgs& a, cudaStream_t st) {
 
 }  // namespace fwd
 
+bool force_simt() {
+  static const bool f = [] {
+    const char* e = getenv("DKV_FORCE_SIMT");
+    return e && e[0] == '1';
+  }();
+  return f;
+}
+
 bool tc_supported(int dtype, int head_dim, int heads, int kv_heads) {
-  if (dtype != DKV_BF16) return false;
+  if (dtype != DKV_BF16 || force_simt()) return false;
   if (head_dim != 64 && head_dim != 128) return false;
   if (kv_heads <= 0 || heads % kv_heads) return false;
   const int G = heads / kv_heads;
