@@ -13,7 +13,10 @@
 //     tile is reduce-added into one fp32 scratch (atomic mode) or stored as
 //     the chunk's partial (deterministic mode) -- then folded and cast once
 //     (kernel.py:279-285, Alg. 1/2).
-// dQ is accumulated across key tiles with fp32 red.global.add into dq_acc.
+// dQ is accumulated across key tiles in fp32: each tile's dQ^T is transposed
+// through shared memory and reduce-added into dq_acc by ONE TMA bulk tensor
+// reduce (cp.reduce.async.bulk.tensor ... add) -- per-lane red.global would
+// be LSU-bound (~1 lane/clk/SM, 8K lanes per query tile).
 //
 // Per query tile (B_q = 64 rows, B_k = 128 keys, d = 128):
 //   S^T  = K Q^T      (M128 N64  K128)  -> TMEM [0,64)
@@ -34,7 +37,7 @@ constexpr int kBK = 128;  // keys per tile (MMA M)
 constexpr int kBQ = 64;   // query rows per tile (MMA N for S^T / dP^T / dQ^T)
 constexpr int D = 128;
 constexpr int kThreads = 320;
-constexpr int kStages = 3;
+constexpr int kStages = 2;
 constexpr int kKVBytes = kBK * D * 2;       // 32 KB
 constexpr int kKVPanel = kBK * 128;         // 16 KB
 constexpr int kQBytes = kBQ * D * 2;        // 16 KB
@@ -47,11 +50,13 @@ constexpr int kOffDO = kOffQ + kStages * kQBytes;
 constexpr int kOffP = kOffDO + kStages * kQBytes;
 constexpr int kOffDS = kOffP + kPBytes;
 constexpr int kOffLD = kOffDS + kPBytes;
-constexpr int kOffBar = kOffLD + kStages * kBQ * 8;
+constexpr int kOffStage = kOffLD + kStages * kBQ * 8;  // dQ staging for the TMA reduce
+constexpr int kStageBytes = kBQ * D * 4;              // 32 KB fp32 tile
+constexpr int kOffBar = kOffStage + 2 * kStageBytes;
 constexpr int kSmemBytes = kOffBar + 512 + 1024;
 
 struct Params {
-  CUtensorMap tm_q, tm_do, tm_k, tm_v, tm_kc, tm_vc;
+  CUtensorMap tm_q, tm_do, tm_k, tm_v, tm_kc, tm_vc, tm_dq;
   const float2* dpack;  // [Hk][T][G] (lse*log2e, D)
   float* dq_acc;        // [T][H][D] f32
   __nv_bfloat16* dk;    // [T][Hk][D]
@@ -183,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     if (lane == 0) {
       tma_prefetch(&p.tm_q);
       tma_prefetch(&p.tm_do);
+      tma_prefetch(&p.tm_dq);
       tma_prefetch(mk);
       tma_prefetch(mv);
       mbar_arrive_expect_tx(&bar.kv_full, 2 * kKVBytes);
@@ -349,14 +355,20 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bar.dq_empty[b]);
-      const int64_t row_tok0 = p.cu[it.s] + it.tok;
+      // transpose through smem ([row][d] fp32) and reduce-add the whole tile with one TMA op
+      float* stg = reinterpret_cast<float*>(base + kOffStage + b * kStageBytes);
+      if (threadIdx.x == 128) bulk_wait_read<1>();  // the reduce issued from this buffer 2 tiles ago
+      named_bar_sync(1, 128);
 #pragma unroll
-      for (int c = 0; c < kBQ; ++c) {
-        const int tl = c / G;
-        if (it.tok + tl < it.rlen)
-          red_add(p.dq_acc + ((row_tok0 + tl) * p.heads + hk * G + c % G) * D + d, __uint_as_float(u[c]));
+      for (int c = 0; c < kBQ; ++c) stg[c * D + d] = __uint_as_float(u[c]);
+      fence_async_smem();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == 128) {
+        tma_reduce_add_3d(&p.tm_dq, stg, 0, hk * G, p.cu[it.s] + it.tok);
+        bulk_commit();
       }
     }
+    if (threadIdx.x == 128) bulk_wait<0>();
   }
 
   // ================= dK / dV epilogue: warps 0-3 dK, warps 4-7 dV (thread = key row)
@@ -438,6 +450,10 @@ int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const float2* dpack, float* 
       set_error("cuTensorMapEncodeTiled failed (backward k_ctx/v_ctx)");
       return DKV_ERR_CUDA;
     }
+  }
+  if (!make_map_3d_f32(&p.tm_dq, dq_acc, a.total_q, a.heads, D, G, tq)) {
+    set_error("cuTensorMapEncodeTiled failed (backward dq_acc)");
+    return DKV_ERR_CUDA;
   }
   p.dpack = dpack;
   p.dq_acc = dq_acc;

@@ -43,4 +43,22 @@ inline bool make_map_3d_bf16(CUtensorMap* m, const void* base, int64_t rows, int
   return r == CUDA_SUCCESS;
 }
 
+// 3-D fp32 map over [rows, heads, dim] (no swizzle), box (dim, box_heads, box_rows);
+// used as the destination of TMA bulk reduce-adds (dQ accumulation).
+inline bool make_map_3d_f32(CUtensorMap* m, const void* base, int64_t rows, int64_t heads, int64_t dim,
+                            uint32_t box_heads, uint32_t box_rows) {
+  std::memset(m, 0, sizeof(*m));
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn || rows <= 0) return false;
+  cuuint64_t gdim[3] = {static_cast<cuuint64_t>(dim), static_cast<cuuint64_t>(heads),
+                        static_cast<cuuint64_t>(rows)};
+  cuuint64_t gstride[2] = {static_cast<cuuint64_t>(dim * 4), static_cast<cuuint64_t>(heads * dim * 4)};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(dim), box_heads, box_rows};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), gdim, gstride, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace dkv

@@ -62,23 +62,43 @@ def test_varlen_forward_bf16_vs_oracle(case, cuda_device):
 
 @pytest.mark.parametrize("case", BF16_CASES, ids=lambda c: f"s{c[0]}")
 def test_backward_bf16_vs_oracle(case, cuda_device):
+    """The backward as a function of (inputs, O, lse, dO): the oracle gets the GPU's own saved
+    O / lse (as the reference's dualkv_bwd takes them, kernel.py:245-293), so D = rowsum(dO*O)
+    is formed from the same bf16 O on both sides."""
     import paper_2605_15422_b200 as dkv
     seed, n, p, rl, h, hk, d = case
     arrs, dev, cu, prec = make_case(seed, n, p, rl, h, hk, d, torch.bfloat16)
     inp, o, lse = _run_dualkv(dev, cu)
     g = dkv.dualkv_bwd(inp, o, lse, dev["do"])
     torch.cuda.synchronize()
-    # oracle backward from the GPU's own saved O / lse would hide forward errors:
-    # use the oracle's forward, as the reference does (kernel.py:213-242)
-    o_ref, lse_ref = orc.dualkv_fwd(arrs["q"], arrs["kc"], arrs["vc"], arrs["kd"], arrs["vd"], cu,
-                                    prec=prec, block_n=128)
-    gr = orc.dualkv_bwd(arrs["q"], arrs["kc"], arrs["vc"], arrs["kd"], arrs["vd"], cu, o_ref, lse_ref,
-                        arrs["do"], prec=prec, block_n=128)
+    gr = orc.dualkv_bwd(arrs["q"], arrs["kc"], arrs["vc"], arrs["kd"], arrs["vd"], cu, to_np(o),
+                        to_np(lse), arrs["do"], prec=prec, block_n=128)
     for got, ref, name in zip(g, gr, ("dQ", "dK_c", "dV_c", "dK_d", "dV_d")):
         if got is None:
             assert ref.size == 0
             continue
         assert_close_bf16(to_np(got), ref, name)
+
+
+@pytest.mark.parametrize("case", BF16_CASES, ids=lambda c: f"s{c[0]}")
+def test_fwd_bwd_bf16_vs_f64_oracle(case, cuda_device):
+    """End to end vs the dense-equivalent f64 oracle: max|gpu - f64| / max|f64| <= 1e-2."""
+    import paper_2605_15422_b200 as dkv
+    seed, n, p, rl, h, hk, d = case
+    arrs, dev, cu, _ = make_case(seed, n, p, rl, h, hk, d, torch.bfloat16)
+    inp, o, lse = _run_dualkv(dev, cu)
+    g = dkv.dualkv_bwd(inp, o, lse, dev["do"])
+    torch.cuda.synchronize()
+    o64, lse64 = orc.dualkv_fwd(arrs["q"], arrs["kc"], arrs["vc"], arrs["kd"], arrs["vd"], cu,
+                                prec="f64", block_n=128)
+    g64 = orc.dualkv_bwd(arrs["q"], arrs["kc"], arrs["vc"], arrs["kd"], arrs["vd"], cu, o64, lse64,
+                         arrs["do"], prec="f64", block_n=128)
+    pairs = [(o, o64, "O")] + list(zip(g, g64, ("dQ", "dK_c", "dV_c", "dK_d", "dV_d")))
+    for got, ref, name in pairs:
+        if ref.size == 0:
+            continue
+        err = np.max(np.abs(to_np(got) - ref)) / max(np.max(np.abs(ref)), 1e-30)
+        assert err <= 1e-2, f"{name}: max err / max|ref| = {err:.3e}"
 
 
 C1 = (11, 4, 256, [128, 128, 128, 128], 8, 8, 64)

@@ -1,0 +1,33 @@
+"""One C3 DualKV step (Call 1 + Call 2, fwd + bwd) for ncu captures.
+
+    ncu --set full --clock-control none --import-source on -k regex:dualkv_bwd -c 1 \
+        -o gpurun_out/prof python tools/profile_step.py
+"""
+
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2605_15422_b200 as dkv  # noqa: E402
+
+n, p, r, h, hk, d = 32, 8192, 2048, 32, 8, 128
+if len(sys.argv) > 1 and sys.argv[1] == "small":
+    n, p, r = 8, 2048, 512
+steps = int(os.environ.get("STEPS", "1"))
+g = torch.Generator(device="cuda").manual_seed(0)
+mk = lambda *s: torch.randn(*s, device="cuda", generator=g).to(torch.bfloat16)
+t = n * r
+qc, kc, vc, doc = mk(p, h, d), mk(p, hk, d), mk(p, hk, d), mk(p, h, d)
+q, kd, vd, dod = mk(t, h, d), mk(t, hk, d), mk(t, hk, d), mk(t, h, d)
+ctx = dkv.VarlenBatch(qc, kc, vc, np.array([0, p]))
+dec = dkv.DualKVInput(q, kc, vc, kd, vd, np.arange(0, t + 1, r))
+for _ in range(steps):
+    oc, lc = dkv.fa2_varlen_fwd(ctx)
+    od, ld = dkv.dualkv_fwd(dec)
+    dkv.dualkv_bwd(dec, od, ld, dod, deterministic=False)
+    dkv.fa2_varlen_bwd(ctx, oc, lc, doc)
+torch.cuda.synchronize()
+print("done")
