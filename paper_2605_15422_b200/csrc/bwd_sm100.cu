@@ -310,7 +310,16 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       // key visible to query column c?
       //   context tile: key < P (all query rows of the chunk see the whole prompt)
       //   own tile:     key <= query token (causal; implies key < R_s for valid rows)
-      const bool key_ok = is_ctx ? key < kv_len : true;
+      // visible columns form a suffix c >= cmin: context keys (< P) are seen by every row; an own
+      // key k is seen by query token t >= k, i.e. columns c >= (k - tok0) * G (rows are token-major)
+      int cmin;
+      if (is_ctx) {
+        cmin = key < kv_len ? 0 : kBQ;
+      } else {
+        const int dt = key - it.tok;
+        cmin = dt <= 0 ? 0 : min(dt * G, kBQ);
+      }
+      const float sl2 = p.scale_log2, sc = p.scale;
       uint32_t pp[32], pd[32];
 #pragma unroll
       for (int c2 = 0; c2 < 32; ++c2) {
@@ -319,12 +328,10 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         for (int h2 = 0; h2 < 2; ++h2) {
           const int c = 2 * c2 + h2;
           const float2 lsd = ld[c];
-          const int qtok = it.tok + c / G;
-          const bool vis = key_ok && (is_ctx || key <= qtok);
-          const float e = ex2(fmaf(__uint_as_float(us[c]), p.scale_log2, -lsd.x));
-          const float pr = vis ? e : 0.f;
+          const float e = ex2(fmaf(__uint_as_float(us[c]), sl2, -lsd.x));
+          const float pr = c >= cmin ? e : 0.f;
           pv[h2] = pr;
-          dv2[h2] = pr * (__uint_as_float(ud[c]) - lsd.y) * p.scale;
+          dv2[h2] = pr * (__uint_as_float(ud[c]) - lsd.y) * sc;
         }
         pp[c2] = pack_bf16(pv[0], pv[1]);
         pd[c2] = pack_bf16(dv2[0], dv2[1]);
