@@ -331,11 +331,13 @@ def main():
     except Exception:
         pass
     peak_burst = peaks.get("bf16_tflops", 1590.0)
+    # per step the main kernels launch twice (Call 2 and Call 1); achieved = their total
+    # algorithmic FLOPs / their total device time (CUDA events around each launch)
+    launches_per_step = 2
     bwd_kernel_ms = bms.value / max(1, bl.value)
     fwd_kernel_ms = fms.value / max(1, fl.value)
-    # per launch: bwd launches alternate Call 2 (decoded) and Call 1 (context); average
-    bwd_flops_per_launch = 10 * pairs(p, [r] * n) * h * d / 2
-    fwd_flops_per_launch = 4 * pairs(p, [r] * n) * h * d / 2
+    bwd_flops_per_launch = 10 * pairs(p, [r] * n) * h * d / launches_per_step
+    fwd_flops_per_launch = 4 * pairs(p, [r] * n) * h * d / launches_per_step
     bwd_ach = bwd_flops_per_launch / (bwd_kernel_ms * 1e-3) / 1e12
     fwd_ach = fwd_flops_per_launch / (fwd_kernel_ms * 1e-3) / 1e12
     roof = {"bound": "tensor", "kernel": "dualkv_bwd_kernel (tcgen05, Call 1 + Call 2 launches averaged)",

@@ -18,7 +18,7 @@ DKV_DEVICE float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(
 // one warp per (token, head).  drow: [H][T] (may be null); dpack: [Hk][T][G] float2
 // (lse * log2(e), D) -- the row order the GQA-packed tensor-core tiles consume.
 template <typename T>
-__global__ void rowsum_kernel(SimtArgs a, float* drow, float* dpack) {
+__global__ void rowsum_kernel(SimtArgs a, float* drow, float* dpack, int tpad) {
   const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= static_cast<int64_t>(a.total_q) * a.heads) return;
@@ -35,22 +35,22 @@ __global__ void rowsum_kernel(SimtArgs a, float* drow, float* dpack) {
     if (dpack) {
       const int G = a.heads / a.kv_heads;
       const int hk = h / G, gi = h % G;
-      const int64_t idx = (static_cast<int64_t>(hk) * a.total_q + t) * G + gi;
+      const int64_t idx = (static_cast<int64_t>(hk) * tpad + t) * G + gi;
       const float lse = a.lse[static_cast<int64_t>(h) * a.total_q + t];
       reinterpret_cast<float2*>(dpack)[idx] = make_float2(lse * 1.4426950408889634f, acc);
     }
   }
 }
 
-void launch_rowsum_do_o(const SimtArgs& a, float* drow, float* dpack, cudaStream_t st) {
+void launch_rowsum_do_o(const SimtArgs& a, float* drow, float* dpack, int tpad, cudaStream_t st) {
   const int64_t warps = static_cast<int64_t>(a.total_q) * a.heads;
   if (warps == 0) return;
   const int threads = 256;
   const int64_t blocks = (warps * 32 + threads - 1) / threads;
   if (a.dtype == DKV_F32)
-    rowsum_kernel<float><<<blocks, threads, 0, st>>>(a, drow, dpack);
+    rowsum_kernel<float><<<blocks, threads, 0, st>>>(a, drow, dpack, tpad);
   else
-    rowsum_kernel<__nv_bfloat16><<<blocks, threads, 0, st>>>(a, drow, dpack);
+    rowsum_kernel<__nv_bfloat16><<<blocks, threads, 0, st>>>(a, drow, dpack, tpad);
 }
 
 // dk/dv[i] = cast(sum_{c < num_parts} partials[c][0/1][i]), fixed chunk order
@@ -78,11 +78,12 @@ void launch_fold_convert(const float* partials, int num_parts, int64_t plane, vo
 }
 
 // vectorised f32 -> {bf16, f32}; RNE via __float2bfloat16_rn (== reference bf16_round)
-__global__ void convert_kernel(const float* __restrict__ src, void* dst, int dtype, int64_t n) {
+__global__ void convert_kernel(const float* __restrict__ src, void* dst, int dtype, int64_t n, float scale) {
   const int64_t i4 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
   if (i4 >= n) return;
   if (i4 + 4 <= n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
     float4 v = *reinterpret_cast<const float4*>(src + i4);
+    v.x *= scale; v.y *= scale; v.z *= scale; v.w *= scale;
     if (dtype == DKV_F32) {
       float* d = static_cast<float*>(dst) + i4;
       d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
@@ -95,17 +96,17 @@ __global__ void convert_kernel(const float* __restrict__ src, void* dst, int dty
   }
   for (int64_t i = i4; i < n && i < i4 + 4; ++i) {
     if (dtype == DKV_F32)
-      static_cast<float*>(dst)[i] = src[i];
+      static_cast<float*>(dst)[i] = src[i] * scale;
     else
-      static_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(src[i]);
+      static_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(src[i] * scale);
   }
 }
 
-void launch_convert(const float* src, void* dst, int dtype, int64_t n, cudaStream_t st) {
+void launch_convert(const float* src, void* dst, int dtype, int64_t n, cudaStream_t st, float scale) {
   if (n == 0) return;
   const int threads = 256;
   const int64_t blocks = ((n + 3) / 4 + threads - 1) / threads;
-  convert_kernel<<<blocks, threads, 0, st>>>(src, dst, dtype, n);
+  convert_kernel<<<blocks, threads, 0, st>>>(src, dst, dtype, n, scale);
 }
 
 // ---------------------------------------------------------------- repack

@@ -37,7 +37,7 @@ constexpr int kBK = 128;  // keys per tile (MMA M)
 constexpr int kBQ = 64;   // query rows per tile (MMA N for S^T / dP^T / dQ^T)
 constexpr int D = 128;
 constexpr int kThreads = 320;
-constexpr int kStages = 2;
+constexpr int kStages = 3;
 constexpr int kKVBytes = kBK * D * 2;       // 32 KB
 constexpr int kKVPanel = kBK * 128;         // 16 KB
 constexpr int kQBytes = kBQ * D * 2;        // 16 KB
@@ -52,18 +52,19 @@ constexpr int kOffDS = kOffP + kPBytes;
 constexpr int kOffLD = kOffDS + kPBytes;
 constexpr int kOffStage = kOffLD + kStages * kBQ * 8;  // dQ staging for the TMA reduce
 constexpr int kStageBytes = kBQ * D * 4;              // 32 KB fp32 tile
-constexpr int kOffBar = kOffStage + 2 * kStageBytes;
-constexpr int kSmemBytes = kOffBar + 512 + 1024;
+constexpr int kOffBar = kOffStage + kStageBytes;
+constexpr int kSmemBytes = kOffBar + 256 + 1024;
+static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory per block");
 
 struct Params {
   CUtensorMap tm_q, tm_do, tm_k, tm_v, tm_kc, tm_vc, tm_dq;
-  const float2* dpack;  // [Hk][T][G] (lse*log2e, D)
+  CUtensorMap tm_ld;    // dpack viewed as [Hk][tpad*G*2] f32: (lse*log2e, D) per (token, head)
   float* dq_acc;        // [T][H][D] f32
   __nv_bfloat16* dk;    // [T][Hk][D]
   __nv_bfloat16* dv;
   float* ctx_acc;       // [parts][2][P][Hk][D]
   const int32_t* cu;
-  int num_seqs, total_q, ctx_len, heads, kv_heads, group, tq;
+  int num_seqs, total_q, ctx_len, heads, kv_heads, group, tq, tpad;
   int chunk, n_ctx_items, n_ctx_tiles;
   int atomic_ctx;
   float scale, scale_log2;
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     mbar_init(&bar.pds_empty, 1);
     mbar_init(&bar.kv_done, 1);
     for (int i = 0; i < kStages; ++i) {
-      mbar_init(&bar.q_full[i], 1 + 32);
+      mbar_init(&bar.q_full[i], 1);
       mbar_init(&bar.q_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -189,6 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       tma_prefetch(&p.tm_q);
       tma_prefetch(&p.tm_do);
       tma_prefetch(&p.tm_dq);
+      tma_prefetch(&p.tm_ld);
       tma_prefetch(mk);
       tma_prefetch(mv);
       mbar_arrive_expect_tx(&bar.kv_full, 2 * kKVBytes);
@@ -198,30 +200,24 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       }
     }
     const uint64_t pol_q = policy_evict_last();
-    QIter it;
-    it.begin(p.cu, p.tq, s0, s1, tok_first);
-    for (int i = 0; it.valid(); it.next(), ++i) {
-      const int st = i % kStages;
-      const uint32_t ph = (i / kStages) & 1;
-      mbar_wait(&bar.q_empty[st], ph ^ 1);
-      const int row0 = p.cu[it.s] + it.tok;
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&bar.q_full[st], 2 * kQBytes);
+    if (lane == 0) {
+      QIter it;
+      it.begin(p.cu, p.tq, s0, s1, tok_first);
+      for (int i = 0; it.valid(); it.next(), ++i) {
+        const int st = i % kStages;
+        const uint32_t ph = (i / kStages) & 1;
+        mbar_wait(&bar.q_empty[st], ph ^ 1);
+        const int row0 = p.cu[it.s] + it.tok;
+        mbar_arrive_expect_tx(&bar.q_full[st], 2 * kQBytes + kBQ * 8);
         for (int pn = 0; pn < 2; ++pn) {
           tma_load_3d_hint(base + kOffQ + st * kQBytes + pn * kQPanel, &p.tm_q, &bar.q_full[st], pn * 64,
                            hk * G, row0, pol_q);
           tma_load_3d_hint(base + kOffDO + st * kQBytes + pn * kQPanel, &p.tm_do, &bar.q_full[st], pn * 64,
                            hk * G, row0, pol_q);
         }
+        // (lse*log2e, D) of the tile's 64 rows: one contiguous 512 B run of dpack
+        tma_load_2d(sLD + st * kBQ, &p.tm_ld, &bar.q_full[st], row0 * G * 2, hk);
       }
-      // (lse*log2e, D) of the 64 rows, rows beyond the sequence end -> (+inf, 0)
-      for (int c = lane; c < kBQ; c += 32) {
-        const int tok = it.tok + c / G;
-        float2 v = make_float2(INFINITY, 0.f);
-        if (tok < it.rlen) v = p.dpack[(static_cast<int64_t>(hk) * p.total_q + p.cu[it.s] + tok) * G + c % G];
-        sLD[st * kBQ + c] = v;
-      }
-      mbar_arrive(&bar.q_full[st]);
     }
   } else if (warp == 9) {
     // ================= MMA issuer
@@ -310,8 +306,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       // key visible to query column c?
       //   context tile: key < P (all query rows of the chunk see the whole prompt)
       //   own tile:     key <= query token (causal; implies key < R_s for valid rows)
-      // visible columns form a suffix c >= cmin: context keys (< P) are seen by every row; an own
-      // key k is seen by query token t >= k, i.e. columns c >= (k - tok0) * G (rows are token-major)
+      // visible columns form a range [cmin, cmax): context keys (< P) are seen by every row of
+      // the sequence; an own key k is seen by query token t >= k, i.e. columns c >= (k - tok0) * G
+      // (rows are token-major); columns past the sequence end are never visible
       int cmin;
       if (is_ctx) {
         cmin = key < kv_len ? 0 : kBQ;
@@ -319,22 +316,32 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         const int dt = key - it.tok;
         cmin = dt <= 0 ? 0 : min(dt * G, kBQ);
       }
-      const float sl2 = p.scale_log2, sc = p.scale;
+      const int cmax = min(kBQ, (it.rlen - it.tok) * G);
+      const float sl2 = p.scale_log2;
       uint32_t pp[32], pd[32];
+      // dS is formed without the softmax scale; it is applied once to dK (epilogue) and dQ (cast)
+      if (__all_sync(0xffffffffu, cmin == 0 && cmax == kBQ)) {
 #pragma unroll
-      for (int c2 = 0; c2 < 32; ++c2) {
-        float pv[2], dv2[2];
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int c = 2 * c2 + h2;
-          const float2 lsd = ld[c];
-          const float e = ex2(fmaf(__uint_as_float(us[c]), sl2, -lsd.x));
-          const float pr = c >= cmin ? e : 0.f;
-          pv[h2] = pr;
-          dv2[h2] = pr * (__uint_as_float(ud[c]) - lsd.y) * sc;
+        for (int c2 = 0; c2 < 32; ++c2) {
+          const float4 lsd = reinterpret_cast<const float4*>(ld)[c2];  // (lse2, D) of columns 2c2, 2c2+1
+          const float e0 = ex2(fmaf(__uint_as_float(us[2 * c2]), sl2, -lsd.x));
+          const float e1 = ex2(fmaf(__uint_as_float(us[2 * c2 + 1]), sl2, -lsd.z));
+          pp[c2] = pack_bf16(e0, e1);
+          pd[c2] = pack_bf16(e0 * (__uint_as_float(ud[2 * c2]) - lsd.y),
+                             e1 * (__uint_as_float(ud[2 * c2 + 1]) - lsd.w));
         }
-        pp[c2] = pack_bf16(pv[0], pv[1]);
-        pd[c2] = pack_bf16(dv2[0], dv2[1]);
+      } else {
+#pragma unroll
+        for (int c2 = 0; c2 < 32; ++c2) {
+          const float4 lsd = reinterpret_cast<const float4*>(ld)[c2];
+          const int c = 2 * c2;
+          float e0 = ex2(fmaf(__uint_as_float(us[c]), sl2, -lsd.x));
+          float e1 = ex2(fmaf(__uint_as_float(us[c + 1]), sl2, -lsd.z));
+          e0 = (c >= cmin && c < cmax) ? e0 : 0.f;
+          e1 = (c + 1 >= cmin && c + 1 < cmax) ? e1 : 0.f;
+          pp[c2] = pack_bf16(e0, e1);
+          pd[c2] = pack_bf16(e0 * (__uint_as_float(ud[c]) - lsd.y), e1 * (__uint_as_float(ud[c + 1]) - lsd.w));
+        }
       }
       mbar_wait(&bar.pds_empty, (i & 1) ^ 1);
 #pragma unroll
@@ -363,8 +370,8 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       tc_fence_before();
       mbar_arrive(&bar.dq_empty[b]);
       // transpose through smem ([row][d] fp32) and reduce-add the whole tile with one TMA op
-      float* stg = reinterpret_cast<float*>(base + kOffStage + b * kStageBytes);
-      if (threadIdx.x == 128) bulk_wait_read<1>();  // the reduce issued from this buffer 2 tiles ago
+      float* stg = reinterpret_cast<float*>(base + kOffStage);
+      if (threadIdx.x == 128) bulk_wait_read<0>();  // the previous tile's reduce has read the staging tile
       named_bar_sync(1, 128);
 #pragma unroll
       for (int c = 0; c < kBQ; ++c) stg[c * D + d] = __uint_as_float(u[c]);
@@ -388,12 +395,15 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     tc_fence_after();
     const int key = kbase + r;
     const bool ok = key < kv_len;
+    const float osc = do_k ? p.scale : 1.f;  // dK = scale * sum dS^T Q
 #pragma unroll 1
     for (int c0 = 0; c0 < D; c0 += 32) {
       uint32_t u[32];
       tmem_ld32(tcol + c0, u);
       tmem_wait_ld();
       if (!ok) continue;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * osc);
       if (is_ctx) {
         const int64_t plane = static_cast<int64_t>(p.ctx_len) * p.kv_heads * D;
         const int chunk_id = s0 / p.chunk;
@@ -438,8 +448,8 @@ bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads) {
   return G <= bwd::kBQ && (bwd::kBQ % G) == 0;
 }
 
-int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const float2* dpack, float* ctx_acc, int chunk, int num_chunks,
-                  bool atomic_ctx, cudaStream_t st) {
+int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const float2* dpack, int tpad, float* ctx_acc, int chunk,
+                  int num_chunks, bool atomic_ctx, cudaStream_t st) {
   using namespace bwd;
   Params p{};
   const int G = a.heads / a.kv_heads;
@@ -462,7 +472,12 @@ int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const float2* dpack, float* 
     set_error("cuTensorMapEncodeTiled failed (backward dq_acc)");
     return DKV_ERR_CUDA;
   }
-  p.dpack = dpack;
+  if (!make_map_2d_f32(&p.tm_ld, dpack, a.kv_heads, static_cast<int64_t>(tpad) * G * 2,
+                       static_cast<int64_t>(tpad) * G * 2, kBQ * 2)) {
+    set_error("cuTensorMapEncodeTiled failed (backward lse/D rows)");
+    return DKV_ERR_CUDA;
+  }
+  p.tpad = tpad;
   p.dq_acc = dq_acc;
   p.dk = static_cast<__nv_bfloat16*>(a.dk);
   p.dv = static_cast<__nv_bfloat16*>(a.dv);

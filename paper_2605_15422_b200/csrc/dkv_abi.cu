@@ -138,6 +138,9 @@ static int auto_chunk(const dkv_bwd_params* p) {
   return static_cast<int>((p->num_seqs + chunks - 1) / chunks);
 }
 
+// dpack row padding: per-KV-head row stride a multiple of 4 tokens (16 B TMA stride)
+static int dpack_tpad(size_t T) { return static_cast<int>((T + 3) & ~size_t(3)); }
+
 struct BwdLayout {
   size_t drow, dpack, dq_acc, ctx, total;
   int chunk, num_chunks, num_parts;
@@ -158,7 +161,7 @@ static BwdLayout bwd_layout(const dkv_bwd_params* p) {
   L.drow = off;
   off += align256(H * T * 4);
   L.dpack = off;
-  off += align256(H * T * 8);
+  off += align256(H * static_cast<size_t>(dpack_tpad(T)) * 8);
   L.dq_acc = off;
   off += tc ? align256(T * H * D * 4) : 0;
   L.ctx = off;
@@ -206,15 +209,18 @@ static int bwd_impl(const dkv_bwd_params* p, void* ws, size_t ws_bytes, bool dua
     const bool atomic_ctx = L.num_parts == 1 && L.num_chunks > 1;
     // chunks whose responses are all empty write nothing: start from zero
     if (plane > 0) cudaMemsetAsync(ctx, 0, static_cast<size_t>(L.num_parts) * 2 * plane * 4, st);
-    launch_rowsum_do_o(a, nullptr, dpack, st);
+    const int tpad = dpack_tpad(static_cast<size_t>(a.total_q));
+    launch_rowsum_do_o(a, nullptr, dpack, tpad, st);
     prof_main_begin(1, st);
-    rc = launch_tc_bwd(a, dq_acc, reinterpret_cast<const float2*>(dpack), ctx, L.chunk, L.num_chunks, atomic_ctx, st);
+    rc = launch_tc_bwd(a, dq_acc, reinterpret_cast<const float2*>(dpack), tpad, ctx, L.chunk, L.num_chunks,
+                       atomic_ctx, st);
     if (rc) return rc;
     prof_main_end(1, st);
-    launch_convert(dq_acc, p->dq, a.dtype, static_cast<int64_t>(a.total_q) * a.heads * a.head_dim, st);
+    // the kernel accumulates dQ / softmax_scale (the scale is folded into this single cast)
+    launch_convert(dq_acc, p->dq, a.dtype, static_cast<int64_t>(a.total_q) * a.heads * a.head_dim, st, a.scale);
     prof_count(3);
   } else {
-    launch_rowsum_do_o(a, drow, nullptr, st);
+    launch_rowsum_do_o(a, drow, nullptr, 0, st);
     prof_main_begin(1, st);
     launch_simt_bwd(a, drow, L.chunk, L.num_chunks, ctx, st);
     prof_main_end(1, st);

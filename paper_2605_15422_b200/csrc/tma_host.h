@@ -61,4 +61,20 @@ inline bool make_map_3d_f32(CUtensorMap* m, const void* base, int64_t rows, int6
   return r == CUDA_SUCCESS;
 }
 
+// 2-D fp32 map over a row-major [rows][cols] buffer (row stride in elements), box (box_cols, 1)
+inline bool make_map_2d_f32(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t stride,
+                            uint32_t box_cols) {
+  std::memset(m, 0, sizeof(*m));
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn || rows <= 0 || cols <= 0) return false;
+  cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t gstride[1] = {static_cast<cuuint64_t>(stride * 4)};
+  cuuint32_t box[2] = {box_cols, 1u};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace dkv

@@ -100,7 +100,8 @@ def _replicated_problem(arrs, cu, p, dt):
 
 
 def _rep_to_dualkv(x, cu, p, which):
-    """Pick decoded rows (which='dec') or sum the prompt rows over copies ('ctx')."""
+    """Pick decoded rows (which='dec') or sum the prompt rows over copies ('ctx'); `cu` holds
+    the DualKV response offsets (copy i occupies P + R_i replicated rows)."""
     parts, acc, off = [], None, 0
     for i in range(len(cu) - 1):
         r = int(cu[i + 1] - cu[i])
@@ -132,10 +133,10 @@ def test_fwd_bwd_bf16_vs_f64_and_replicated(case, cuda_device):
                                 prec="f64", block_n=128)
     g64 = orc.dualkv_bwd(arrs["q"], arrs["kc"], arrs["vc"], arrs["kd"], arrs["vd"], cu, o64, lse64,
                          arrs["do"], prec="f64", block_n=128)
-    rep = [_rep_to_dualkv(to_np(o_r), cur, p, "dec"), _rep_to_dualkv(to_np(gq_r), cur, p, "dec"),
-           _rep_to_dualkv(to_np(gk_r), cur, p, "ctx") if p else np.zeros((0, hk, d)),
-           _rep_to_dualkv(to_np(gv_r), cur, p, "ctx") if p else np.zeros((0, hk, d)),
-           _rep_to_dualkv(to_np(gk_r), cur, p, "dec"), _rep_to_dualkv(to_np(gv_r), cur, p, "dec")]
+    rep = [_rep_to_dualkv(to_np(o_r), cu, p, "dec"), _rep_to_dualkv(to_np(gq_r), cu, p, "dec"),
+           _rep_to_dualkv(to_np(gk_r), cu, p, "ctx") if p else np.zeros((0, hk, d)),
+           _rep_to_dualkv(to_np(gv_r), cu, p, "ctx") if p else np.zeros((0, hk, d)),
+           _rep_to_dualkv(to_np(gk_r), cu, p, "dec"), _rep_to_dualkv(to_np(gv_r), cu, p, "dec")]
     ours = [o] + list(g)
     names = ("O", "dQ", "dK_c", "dV_c", "dK_d", "dV_d")
     toy = sum(rl) * (p + 1) < 64
