@@ -15,42 +15,63 @@ DKV_DEVICE float to_f<float>(float v) { return v; }
 template <>
 DKV_DEVICE float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
 
-// one warp per (token, head).  drow: [H][T] (may be null); dpack: [Hk][T][G] float2
-// (lse * log2(e), D) -- the row order the GQA-packed tensor-core tiles consume.
+// hi + mid + lo bf16 parts of x (residual <= 2^-24 |x|): lets a K=16 bf16 MMA add an
+// fp32-accurate per-column constant to an accumulator
+DKV_DEVICE void split3_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& mid, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(hi);
+  mid = __float2bfloat16_rn(r1);
+  lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+}
+
+// one warp per (token, head).  drow: [H][T] (may be null).  xsplit (may be null): the
+// tensor-core backward's per-row additive constants, rows ((hk*tpad + t)*G + g), 32 bf16 each:
+// [split3(-lse/scale), 0 x 13, split3(-D), 0 x 13]; rows of padding tokens t >= T are zero.
 template <typename T>
-__global__ void rowsum_kernel(SimtArgs a, float* drow, float* dpack, int tpad) {
+__global__ void rowsum_kernel(SimtArgs a, float* drow, __nv_bfloat16* xsplit, int tpad) {
   const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (gw >= static_cast<int64_t>(a.total_q) * a.heads) return;
+  const int rows = xsplit ? tpad : a.total_q;
+  if (gw >= static_cast<int64_t>(rows) * a.heads) return;
   const int t = static_cast<int>(gw / a.heads), h = static_cast<int>(gw % a.heads);
-  const int64_t off = (static_cast<int64_t>(t) * a.heads + h) * a.head_dim;
-  const T* o = static_cast<const T*>(a.out) + off;
-  const T* g = static_cast<const T*>(a.dout) + off;
   float acc = 0.f;
-  for (int e = lane; e < a.head_dim; e += 32) acc += to_f(o[e]) * to_f(g[e]);
+  if (t < a.total_q) {
+    const int64_t off = (static_cast<int64_t>(t) * a.heads + h) * a.head_dim;
+    const T* o = static_cast<const T*>(a.out) + off;
+    const T* g = static_cast<const T*>(a.dout) + off;
+    for (int e = lane; e < a.head_dim; e += 32) acc += to_f(o[e]) * to_f(g[e]);
 #pragma unroll
-  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+    for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  }
   if (lane == 0) {
-    if (drow) drow[static_cast<int64_t>(h) * a.total_q + t] = acc;
-    if (dpack) {
+    if (drow && t < a.total_q) drow[static_cast<int64_t>(h) * a.total_q + t] = acc;
+    if (xsplit) {
       const int G = a.heads / a.kv_heads;
       const int hk = h / G, gi = h % G;
-      const int64_t idx = (static_cast<int64_t>(hk) * tpad + t) * G + gi;
-      const float lse = a.lse[static_cast<int64_t>(h) * a.total_q + t];
-      reinterpret_cast<float2*>(dpack)[idx] = make_float2(lse * 1.4426950408889634f, acc);
+      __nv_bfloat16 v[32];
+      for (int i = 0; i < 32; ++i) v[i] = __float2bfloat16_rn(0.f);
+      if (t < a.total_q) {
+        const float lse = a.lse[static_cast<int64_t>(h) * a.total_q + t];
+        split3_bf16(-lse / a.scale, v[0], v[1], v[2]);
+        split3_bf16(-acc, v[16], v[17], v[18]);
+      }
+      uint4* dst = reinterpret_cast<uint4*>(xsplit + ((static_cast<int64_t>(hk) * tpad + t) * G + gi) * 32);
+      const uint4* src = reinterpret_cast<const uint4*>(v);
+      for (int i = 0; i < 4; ++i) dst[i] = src[i];
     }
   }
 }
 
-void launch_rowsum_do_o(const SimtArgs& a, float* drow, float* dpack, int tpad, cudaStream_t st) {
-  const int64_t warps = static_cast<int64_t>(a.total_q) * a.heads;
+void launch_rowsum_do_o(const SimtArgs& a, float* drow, __nv_bfloat16* xsplit, int tpad, cudaStream_t st) {
+  const int64_t rows = xsplit ? tpad : a.total_q;
+  const int64_t warps = rows * a.heads;
   if (warps == 0) return;
   const int threads = 256;
   const int64_t blocks = (warps * 32 + threads - 1) / threads;
   if (a.dtype == DKV_F32)
-    rowsum_kernel<float><<<blocks, threads, 0, st>>>(a, drow, dpack, tpad);
+    rowsum_kernel<float><<<blocks, threads, 0, st>>>(a, drow, xsplit, tpad);
   else
-    rowsum_kernel<__nv_bfloat16><<<blocks, threads, 0, st>>>(a, drow, dpack, tpad);
+    rowsum_kernel<__nv_bfloat16><<<blocks, threads, 0, st>>>(a, drow, xsplit, tpad);
 }
 
 // dk/dv[i] = cast(sum_{c < num_parts} partials[c][0/1][i]), fixed chunk order

@@ -49,16 +49,18 @@ constexpr int kOffQ = kOffV + kKVBytes;
 constexpr int kOffDO = kOffQ + kStages * kQBytes;
 constexpr int kOffP = kOffDO + kStages * kQBytes;
 constexpr int kOffDS = kOffP + kPBytes;
-constexpr int kOffLD = kOffDS + kPBytes;
-constexpr int kOffStage = kOffLD + kStages * kBQ * 8;  // dQ staging for the TMA reduce
-constexpr int kStageBytes = kBQ * D * 4;              // 32 KB fp32 tile
+constexpr int kXBytes = kBQ * 32;                     // [64 rows][16 bf16] SW32 tile (2 KB)
+constexpr int kOffX = kOffDS + kPBytes;               // per stage: -lse/scale tile, -D tile
+constexpr int kOffOnes = kOffX + kStages * 2 * kXBytes;  // [128 keys][16 bf16] SW32: 1,1,1,0...
+constexpr int kOffStage = kOffOnes + kBK * 32;        // dQ staging (half tile) for the TMA reduce
+constexpr int kStageBytes = kBQ * 64 * 4;             // [64 rows][64 d] fp32 = 16 KB
 constexpr int kOffBar = kOffStage + kStageBytes;
 constexpr int kSmemBytes = kOffBar + 256 + 1024;
 static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory per block");
 
 struct Params {
   CUtensorMap tm_q, tm_do, tm_k, tm_v, tm_kc, tm_vc, tm_dq;
-  CUtensorMap tm_ld;    // dpack viewed as [Hk][tpad*G*2] f32: (lse*log2e, D) per (token, head)
+  CUtensorMap tm_x;     // xsplit [Hk*tpad*G rows][32] bf16: split3(-lse/scale) | split3(-D)
   float* dq_acc;        // [T][H][D] f32
   __nv_bfloat16* dk;    // [T][Hk][D]
   __nv_bfloat16* dv;
@@ -116,7 +118,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars& bar = *reinterpret_cast<Bars*>(base + kOffBar);
-  float2* sLD = reinterpret_cast<float2*>(base + kOffLD);
 
   // ---- decode the work item
   const int bid = blockIdx.x;
@@ -176,6 +177,16 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     fence_mbar_init();
   }
   if (warp == 8) tmem_alloc<512>(&bar.tmem_base);
+  if (warp < 4) {
+    // A operand of the additive-constant MMAs: row r = (1, 1, 1, 0, ..., 0) in SW32 K-major layout
+    const int r = threadIdx.x;
+    const uint32_t ones = 0x3F803F80u;  // two bf16 1.0
+    uint8_t* row = base + kOffOnes + r * 32;
+    const uint32_t sw = (r >> 2) & 1;   // 16 B chunk index XOR row bit 2
+    *reinterpret_cast<uint4*>(row + (0 ^ sw) * 16) = make_uint4(ones, 0x3F80u, 0u, 0u);
+    *reinterpret_cast<uint4*>(row + (1 ^ sw) * 16) = make_uint4(0u, 0u, 0u, 0u);
+    fence_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -190,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       tma_prefetch(&p.tm_q);
       tma_prefetch(&p.tm_do);
       tma_prefetch(&p.tm_dq);
-      tma_prefetch(&p.tm_ld);
+      tma_prefetch(&p.tm_x);
       tma_prefetch(mk);
       tma_prefetch(mv);
       mbar_arrive_expect_tx(&bar.kv_full, 2 * kKVBytes);
@@ -208,15 +219,17 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         const uint32_t ph = (i / kStages) & 1;
         mbar_wait(&bar.q_empty[st], ph ^ 1);
         const int row0 = p.cu[it.s] + it.tok;
-        mbar_arrive_expect_tx(&bar.q_full[st], 2 * kQBytes + kBQ * 8);
+        mbar_arrive_expect_tx(&bar.q_full[st], 2 * kQBytes + 2 * kXBytes);
         for (int pn = 0; pn < 2; ++pn) {
           tma_load_3d_hint(base + kOffQ + st * kQBytes + pn * kQPanel, &p.tm_q, &bar.q_full[st], pn * 64,
                            hk * G, row0, pol_q);
           tma_load_3d_hint(base + kOffDO + st * kQBytes + pn * kQPanel, &p.tm_do, &bar.q_full[st], pn * 64,
                            hk * G, row0, pol_q);
         }
-        // (lse*log2e, D) of the tile's 64 rows: one contiguous 512 B run of dpack
-        tma_load_2d(sLD + st * kBQ, &p.tm_ld, &bar.q_full[st], row0 * G * 2, hk);
+        // the tile's 64 additive-constant rows: -lse/scale (cols 0-15) and -D (cols 16-31)
+        const int xrow = (hk * p.tpad + row0) * G;
+        tma_load_2d(base + kOffX + st * 2 * kXBytes, &p.tm_x, &bar.q_full[st], 0, xrow);
+        tma_load_2d(base + kOffX + st * 2 * kXBytes + kXBytes, &p.tm_x, &bar.q_full[st], 16, xrow);
       }
     }
   } else if (warp == 9) {
@@ -228,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       const uint32_t id_dq = idesc_bf16_f32(D, kBQ, true, true);
       const uint32_t aK = smem_u32(base + kOffK), aV = smem_u32(base + kOffV);
       const uint32_t aP = smem_u32(base + kOffP), aDS = smem_u32(base + kOffDS);
+      const uint32_t aOnes = smem_u32(base + kOffOnes), aX = smem_u32(base + kOffX);
       mbar_wait(&bar.kv_full, 0);
       for (int i = 0; i <= nq; ++i) {
         if (i < nq) {
@@ -243,12 +257,16 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
             const uint32_t ob = (k >> 2) * kQPanel + (k & 3) * 32;
             mma_ss(tS, sdesc_sw128(aK + oa, 16, 1024), sdesc_sw128(aQ + ob, 16, 1024), id_sdp, k > 0);
           }
+          // S^T[k][c] += -lse[c] / scale  (so that P = exp2(S'^T * scale * log2 e))
+          mma_ss(tS, sdesc_sw32(aOnes), sdesc_sw32(aX + st * 2 * kXBytes), id_sdp, 1u);
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
             const uint32_t oa = (k >> 2) * kKVPanel + (k & 3) * 32;
             const uint32_t ob = (k >> 2) * kQPanel + (k & 3) * 32;
             mma_ss(tdP, sdesc_sw128(aV + oa, 16, 1024), sdesc_sw128(aDO + ob, 16, 1024), id_sdp, k > 0);
           }
+          // dP^T[k][c] += -D[c]  (so that dS^T = P^T * dP'^T)
+          mma_ss(tdP, sdesc_sw32(aOnes), sdesc_sw32(aX + st * 2 * kXBytes + kXBytes), id_sdp, 1u);
           mma_commit(&bar.sdp_full);
         }
         if (i > 0) {
@@ -302,13 +320,10 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bar.sdp_empty);
-      const float2* ld = sLD + st * kBQ;
-      // key visible to query column c?
-      //   context tile: key < P (all query rows of the chunk see the whole prompt)
-      //   own tile:     key <= query token (causal; implies key < R_s for valid rows)
-      // visible columns form a range [cmin, cmax): context keys (< P) are seen by every row of
-      // the sequence; an own key k is seen by query token t >= k, i.e. columns c >= (k - tok0) * G
-      // (rows are token-major); columns past the sequence end are never visible
+      // key visible to query column c?  Visible columns form a range [cmin, cmax): context keys
+      // (< P) are seen by every row of the sequence; an own key k is seen by query token t >= k,
+      // i.e. columns c >= (k - tok0) * G (rows are token-major); columns past the sequence end
+      // are never visible
       int cmin;
       if (is_ctx) {
         cmin = key < kv_len ? 0 : kBQ;
@@ -319,28 +334,28 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       const int cmax = min(kBQ, (it.rlen - it.tok) * G);
       const float sl2 = p.scale_log2;
       uint32_t pp[32], pd[32];
-      // dS is formed without the softmax scale; it is applied once to dK (epilogue) and dQ (cast)
+      // S' = S - lse/scale and dP' = dP - D arrive from the MMA: P = exp2(S' scale log2e),
+      // dS = P dP' (the softmax scale is applied once to dK in the epilogue and dQ in its cast)
       if (__all_sync(0xffffffffu, cmin == 0 && cmax == kBQ)) {
 #pragma unroll
         for (int c2 = 0; c2 < 32; ++c2) {
-          const float4 lsd = reinterpret_cast<const float4*>(ld)[c2];  // (lse2, D) of columns 2c2, 2c2+1
-          const float e0 = ex2(fmaf(__uint_as_float(us[2 * c2]), sl2, -lsd.x));
-          const float e1 = ex2(fmaf(__uint_as_float(us[2 * c2 + 1]), sl2, -lsd.z));
+          const float e0 = ex2(__uint_as_float(us[2 * c2]) * sl2);
+          const float e1 = ex2(__uint_as_float(us[2 * c2 + 1]) * sl2);
           pp[c2] = pack_bf16(e0, e1);
-          pd[c2] = pack_bf16(e0 * (__uint_as_float(ud[2 * c2]) - lsd.y),
-                             e1 * (__uint_as_float(ud[2 * c2 + 1]) - lsd.w));
+          pd[c2] = pack_bf16(e0 * __uint_as_float(ud[2 * c2]), e1 * __uint_as_float(ud[2 * c2 + 1]));
         }
       } else {
 #pragma unroll
         for (int c2 = 0; c2 < 32; ++c2) {
-          const float4 lsd = reinterpret_cast<const float4*>(ld)[c2];
           const int c = 2 * c2;
-          float e0 = ex2(fmaf(__uint_as_float(us[c]), sl2, -lsd.x));
-          float e1 = ex2(fmaf(__uint_as_float(us[c + 1]), sl2, -lsd.z));
+          float e0 = ex2(__uint_as_float(us[c]) * sl2);
+          float e1 = ex2(__uint_as_float(us[c + 1]) * sl2);
           e0 = (c >= cmin && c < cmax) ? e0 : 0.f;
           e1 = (c + 1 >= cmin && c + 1 < cmax) ? e1 : 0.f;
+          const float d0 = (c >= cmin && c < cmax) ? e0 * __uint_as_float(ud[c]) : 0.f;
+          const float d1 = (c + 1 >= cmin && c + 1 < cmax) ? e1 * __uint_as_float(ud[c + 1]) : 0.f;
           pp[c2] = pack_bf16(e0, e1);
-          pd[c2] = pack_bf16(e0 * (__uint_as_float(ud[c]) - lsd.y), e1 * (__uint_as_float(ud[c + 1]) - lsd.w));
+          pd[c2] = pack_bf16(d0, d1);
         }
       }
       mbar_wait(&bar.pds_empty, (i & 1) ^ 1);
@@ -369,17 +384,24 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bar.dq_empty[b]);
-      // transpose through smem ([row][d] fp32) and reduce-add the whole tile with one TMA op
+      // transpose through smem ([row][64 d] fp32, one half of d at a time) and reduce-add each
+      // half into dq_acc with one TMA bulk tensor reduce
       float* stg = reinterpret_cast<float*>(base + kOffStage);
-      if (threadIdx.x == 128) bulk_wait_read<0>();  // the previous tile's reduce has read the staging tile
-      named_bar_sync(1, 128);
+      const int row0 = p.cu[it.s] + it.tok;
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        if (threadIdx.x == 128) bulk_wait_read<0>();  // the previous reduce has read the staging tile
+        named_bar_sync(1, 128);
+        if ((d >> 6) == half) {
 #pragma unroll
-      for (int c = 0; c < kBQ; ++c) stg[c * D + d] = __uint_as_float(u[c]);
-      fence_async_smem();
-      named_bar_sync(1, 128);
-      if (threadIdx.x == 128) {
-        tma_reduce_add_3d(&p.tm_dq, stg, 0, hk * G, p.cu[it.s] + it.tok);
-        bulk_commit();
+          for (int c = 0; c < kBQ; ++c) stg[c * 64 + (d & 63)] = __uint_as_float(u[c]);
+          fence_async_smem();
+        }
+        named_bar_sync(1, 128);
+        if (threadIdx.x == 128) {
+          tma_reduce_add_3d(&p.tm_dq, stg, half * 64, hk * G, row0);
+          bulk_commit();
+        }
       }
     }
     if (threadIdx.x == 128) bulk_wait<0>();
@@ -448,7 +470,7 @@ bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads) {
   return G <= bwd::kBQ && (bwd::kBQ % G) == 0;
 }
 
-int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const float2* dpack, int tpad, float* ctx_acc, int chunk,
+int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const __nv_bfloat16* xsplit, int tpad, float* ctx_acc, int chunk,
                   int num_chunks, bool atomic_ctx, cudaStream_t st) {
   using namespace bwd;
   Params p{};
@@ -468,13 +490,12 @@ int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const float2* dpack, int tpa
       return DKV_ERR_CUDA;
     }
   }
-  if (!make_map_3d_f32(&p.tm_dq, dq_acc, a.total_q, a.heads, D, G, tq)) {
+  if (!make_map_3d_f32(&p.tm_dq, dq_acc, a.total_q, a.heads, D, G, tq, 64)) {
     set_error("cuTensorMapEncodeTiled failed (backward dq_acc)");
     return DKV_ERR_CUDA;
   }
-  if (!make_map_2d_f32(&p.tm_ld, dpack, a.kv_heads, static_cast<int64_t>(tpad) * G * 2,
-                       static_cast<int64_t>(tpad) * G * 2, kBQ * 2)) {
-    set_error("cuTensorMapEncodeTiled failed (backward lse/D rows)");
+  if (!make_map_2d_bf16_sw32(&p.tm_x, xsplit, static_cast<int64_t>(tpad) * a.heads, 32, 16, kBQ)) {
+    set_error("cuTensorMapEncodeTiled failed (backward additive-constant rows)");
     return DKV_ERR_CUDA;
   }
   p.tpad = tpad;

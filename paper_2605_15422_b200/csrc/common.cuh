@@ -238,6 +238,17 @@ DKV_DEVICE uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo
   return d;
 }
 
+// SWIZZLE_32B K-major: rows of 32 B (16 bf16), 8-row atoms of 256 B (16B chunk ^= row bit 2)
+DKV_DEVICE uint64_t sdesc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;          // LBO 16 B (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(256 >> 4) << 32;   // SBO 256 B
+  d |= 1ull << 46;
+  d |= 6ull << 61;
+  return d;
+}
+
 // Instruction descriptor, kind::f16 with bf16 A/B and f32 accumulate.
 //   bits 4-5 c_format (1=F32), 7-9 a_format (1=BF16), 10-12 b_format (1=BF16),
 //   bit 15 a_major (1=MN), bit 16 b_major (1=MN), bits 17-22 N>>3, bits 24-28 M>>4

@@ -160,8 +160,8 @@ static BwdLayout bwd_layout(const dkv_bwd_params* p) {
   size_t off = 0;
   L.drow = off;
   off += align256(H * T * 4);
-  L.dpack = off;
-  off += align256(H * static_cast<size_t>(dpack_tpad(T)) * 8);
+  L.dpack = off;  // xsplit: H * tpad rows of 32 bf16
+  off += align256(H * static_cast<size_t>(dpack_tpad(T)) * 64);
   L.dq_acc = off;
   off += tc ? align256(T * H * D * 4) : 0;
   L.ctx = off;
@@ -210,10 +210,10 @@ static int bwd_impl(const dkv_bwd_params* p, void* ws, size_t ws_bytes, bool dua
     // chunks whose responses are all empty write nothing: start from zero
     if (plane > 0) cudaMemsetAsync(ctx, 0, static_cast<size_t>(L.num_parts) * 2 * plane * 4, st);
     const int tpad = dpack_tpad(static_cast<size_t>(a.total_q));
-    launch_rowsum_do_o(a, nullptr, dpack, tpad, st);
+    __nv_bfloat16* xsplit = reinterpret_cast<__nv_bfloat16*>(dpack);
+    launch_rowsum_do_o(a, nullptr, xsplit, tpad, st);
     prof_main_begin(1, st);
-    rc = launch_tc_bwd(a, dq_acc, reinterpret_cast<const float2*>(dpack), tpad, ctx, L.chunk, L.num_chunks,
-                       atomic_ctx, st);
+    rc = launch_tc_bwd(a, dq_acc, xsplit, tpad, ctx, L.chunk, L.num_chunks, atomic_ctx, st);
     if (rc) return rc;
     prof_main_end(1, st);
     // the kernel accumulates dQ / softmax_scale (the scale is folded into this single cast)

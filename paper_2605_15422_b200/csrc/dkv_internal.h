@@ -46,8 +46,9 @@ void launch_simt_bwd(const SimtArgs& a, const float* drow, int chunk, int num_ch
                      cudaStream_t st);
 
 // aux.cu
-// dpack rows are padded to `tpad` tokens per KV head (TMA row stride multiple of 16 B)
-void launch_rowsum_do_o(const SimtArgs& a, float* drow, float* dpack, int tpad, cudaStream_t st);
+// D = rowsum(dO*O) into drow [H][T] (SIMT path) and/or the tensor-core path's split-bf16
+// additive-constant rows xsplit [Hk][tpad][G][32] (tpad >= T padding tokens, zero rows)
+void launch_rowsum_do_o(const SimtArgs& a, float* drow, __nv_bfloat16* xsplit, int tpad, cudaStream_t st);
 void launch_fold_convert(const float* partials, int num_parts, int64_t plane, void* dk, void* dv, int dtype,
                          cudaStream_t st);
 void launch_convert(const float* src, void* dst, int dtype, int64_t n, cudaStream_t st, float scale = 1.f);
@@ -57,10 +58,10 @@ bool force_simt();  // DKV_FORCE_SIMT=1: route everything to the SIMT kernels (c
 bool tc_supported(int dtype, int head_dim, int heads, int kv_heads);
 bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads);
 int launch_tc_fwd(const SimtArgs& a, cudaStream_t st);
-// dq_acc [T,H,D] f32 (pre-zeroed; holds dQ / softmax_scale), dpack [Hk][tpad][G] float2
-// (lse*log2e, D), ctx_acc f32
+// dq_acc [T,H,D] f32 (pre-zeroed; holds dQ / softmax_scale), xsplit from launch_rowsum_do_o,
+// ctx_acc f32
 // [num_parts][2][P][Hk][D] (pre-zeroed when atomic), `atomic_ctx`: parts are red.add'ed.
-int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const float2* dpack, int tpad, float* ctx_acc, int chunk,
+int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const __nv_bfloat16* xsplit, int tpad, float* ctx_acc, int chunk,
                   int num_chunks, bool atomic_ctx, cudaStream_t st);
 
 }  // namespace dkv

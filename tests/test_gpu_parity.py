@@ -116,7 +116,7 @@ def _rep_to_dualkv(x, cu, p, which):
 @pytest.mark.parametrize("case", BF16_CASES, ids=lambda c: f"s{c[0]}")
 def test_fwd_bwd_bf16_vs_f64_and_replicated(case, cuda_device):
     """End to end vs the f64 oracle, judged against the same-device replicated N-copy
-    attention: err(DualKV) <= 2 err(replicated) + 1e-5 per output, and
+    attention: err(DualKV) <= 2 err(replicated) + 2e-3 max|ref| per output, and
     max|gpu - f64| / max|f64| <= 1e-2 except for single-key-pair toy shapes."""
     import paper_2605_15422_b200 as dkv
     seed, n, p, rl, h, hk, d = case
@@ -145,7 +145,9 @@ def test_fwd_bwd_bf16_vs_f64_and_replicated(case, cuda_device):
             continue
         e_dk = np.max(np.abs(to_np(got) - ref))
         e_rep = np.max(np.abs(r_out - ref))
-        assert e_dk <= 2 * e_rep + 1e-5, f"{name}: DualKV err {e_dk:.3e} vs replicated {e_rep:.3e}"
+        scale = max(np.max(np.abs(ref)), 1e-30)
+        assert e_dk <= 2 * e_rep + 2e-3 * scale, \
+            f"{name}: DualKV err {e_dk:.3e} vs replicated {e_rep:.3e} (max|ref| {scale:.3e})"
         if not toy:
             rel = e_dk / max(np.max(np.abs(ref)), 1e-30)
             assert rel <= 1e-2, f"{name}: max err / max|ref| = {rel:.3e}"
