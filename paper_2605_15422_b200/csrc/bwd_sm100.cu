@@ -22,9 +22,11 @@
 //   S^T  = K Q^T      (M128 N64  K128)  -> TMEM [0,64)
 //   dP^T = V dO^T     (M128 N64  K128)  -> TMEM [64,128)
 //   P^T = exp2(S^T*scale*log2e - lse2), dS^T = P^T (dP^T - D) * scale   (compute WG)
-//   dV  += P^T dO     (M128 N128 K64)   A = P^T (smem)   -> TMEM [256,384)
-//   dK  += dS^T Q     (M128 N128 K64)   A = dS^T (smem)  -> TMEM [384,512)
-//   dQ^T = K^T dS^T   (M128 N64  K128)  double-buffered  -> TMEM [128,256)
+//   S^T += 1 (-lse/scale)^T, dP^T += 1 (-D)^T  (K=16 split-bf16 MMAs: no per-column loads)
+//   P^T, dS^T (bf16) -> TMEM [128,160), [160,192); dS^T also -> smem
+//   dV  += P^T dO     (M128 N128 K64)   TS-MMA, A = P^T (TMEM)  -> TMEM [256,384)
+//   dK  += dS^T Q     (M128 N128 K64)   TS-MMA, A = dS^T (TMEM) -> TMEM [384,512)
+//   dQ^T = K^T dS^T   (M128 N64  K128)  SS-MMA                  -> TMEM [192,256)
 // Roles: warps 0-3 compute (thread = key row), 4-7 dQ drain (thread = head-dim
 // lane) + dV epilogue, 8 TMA producer + TMEM allocator, 9 MMA issuer.
 #include "dkv_internal.h"
@@ -47,13 +49,12 @@ constexpr int kOffK = 0;
 constexpr int kOffV = kOffK + kKVBytes;
 constexpr int kOffQ = kOffV + kKVBytes;
 constexpr int kOffDO = kOffQ + kStages * kQBytes;
-constexpr int kOffP = kOffDO + kStages * kQBytes;
-constexpr int kOffDS = kOffP + kPBytes;
+constexpr int kOffDS = kOffDO + kStages * kQBytes;
 constexpr int kXBytes = kBQ * 32;                     // [64 rows][16 bf16] SW32 tile (2 KB)
 constexpr int kOffX = kOffDS + kPBytes;               // per stage: -lse/scale tile, -D tile
 constexpr int kOffOnes = kOffX + kStages * 2 * kXBytes;  // [128 keys][16 bf16] SW32: 1,1,1,0...
-constexpr int kOffStage = kOffOnes + kBK * 32;        // dQ staging (half tile) for the TMA reduce
-constexpr int kStageBytes = kBQ * 64 * 4;             // [64 rows][64 d] fp32 = 16 KB
+constexpr int kOffStage = kOffOnes + kBK * 32;        // dQ staging tile for the TMA reduce
+constexpr int kStageBytes = kBQ * D * 4;              // [64 rows][128 d] fp32 = 32 KB
 constexpr int kOffBar = kOffStage + kStageBytes;
 constexpr int kSmemBytes = kOffBar + 256 + 1024;
 static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory per block");
@@ -75,7 +76,7 @@ struct Params {
 struct Bars {
   uint64_t kv_full, sdp_full, sdp_empty, pds_full, pds_empty, kv_done;
   uint64_t q_full[kStages], q_empty[kStages];
-  uint64_t dq_full[2], dq_empty[2];
+  uint64_t dq_full, dq_empty;
   uint32_t tmem_base;
 };
 
@@ -170,10 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       mbar_init(&bar.q_full[i], 1);
       mbar_init(&bar.q_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bar.dq_full[i], 1);
-      mbar_init(&bar.dq_empty[i], 128);
-    }
+    mbar_init(&bar.dq_full, 1);
+    mbar_init(&bar.dq_empty, 128);
     fence_mbar_init();
   }
   if (warp == 8) tmem_alloc<512>(&bar.tmem_base);
@@ -235,12 +234,13 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
   } else if (warp == 9) {
     // ================= MMA issuer
     if (elect_one()) {
-      const uint32_t tS = tmem, tdP = tmem + 64, tdQ = tmem + 128, tdV = tmem + 256, tdK = tmem + 384;
+      const uint32_t tS = tmem, tdP = tmem + 64, tP = tmem + 128, tDS = tmem + 160, tdQ = tmem + 192;
+      const uint32_t tdV = tmem + 256, tdK = tmem + 384;
       const uint32_t id_sdp = idesc_bf16_f32(kBK, kBQ, false, false);
       const uint32_t id_kv = idesc_bf16_f32(kBK, D, false, true);
       const uint32_t id_dq = idesc_bf16_f32(D, kBQ, true, true);
       const uint32_t aK = smem_u32(base + kOffK), aV = smem_u32(base + kOffV);
-      const uint32_t aP = smem_u32(base + kOffP), aDS = smem_u32(base + kOffDS);
+      const uint32_t aDS = smem_u32(base + kOffDS);
       const uint32_t aOnes = smem_u32(base + kOffOnes), aX = smem_u32(base + kOffX);
       mbar_wait(&bar.kv_full, 0);
       for (int i = 0; i <= nq; ++i) {
@@ -278,21 +278,18 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < kBQ / 16; ++k)
-            mma_ss(tdV, sdesc_sw128(aP + k * 32, 16, 1024), sdesc_sw128(aDO + k * 2048, kQPanel, 1024), id_kv,
-                   (j > 0 || k > 0) ? 1u : 0u);
+            mma_ts(tdV, tP + k * 8, sdesc_sw128(aDO + k * 2048, kQPanel, 1024), id_kv, (j > 0 || k > 0) ? 1u : 0u);
 #pragma unroll
           for (int k = 0; k < kBQ / 16; ++k)
-            mma_ss(tdK, sdesc_sw128(aDS + k * 32, 16, 1024), sdesc_sw128(aQ + k * 2048, kQPanel, 1024), id_kv,
-                   (j > 0 || k > 0) ? 1u : 0u);
+            mma_ts(tdK, tDS + k * 8, sdesc_sw128(aQ + k * 2048, kQPanel, 1024), id_kv, (j > 0 || k > 0) ? 1u : 0u);
           mma_commit(&bar.q_empty[sj]);
-          const int b = j & 1;
-          mbar_wait(&bar.dq_empty[b], ((j >> 1) & 1) ^ 1);
+          mbar_wait(&bar.dq_empty, (j & 1) ^ 1);
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
-            mma_ss(tdQ + b * 64, sdesc_sw128(aK + k * 2048, kKVPanel, 1024), sdesc_sw128(aDS + k * 2048, kPBytes, 1024),
+            mma_ss(tdQ, sdesc_sw128(aK + k * 2048, kKVPanel, 1024), sdesc_sw128(aDS + k * 2048, kPBytes, 1024),
                    id_dq, k > 0);
-          mma_commit(&bar.dq_full[b]);
+          mma_commit(&bar.dq_full);
           mma_commit(&bar.pds_empty);
         }
       }
@@ -303,7 +300,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     const int r = warp * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     const int key = kbase + r;  // region-local key index
-    uint8_t* sP = base + kOffP;
     uint8_t* sDS = base + kOffDS;
     QIter it;
     it.begin(p.cu, p.tq, s0, s1, tok_first);
@@ -359,12 +355,17 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         }
       }
       mbar_wait(&bar.pds_empty, (i & 1) ^ 1);
+      tc_fence_after();
+      // P^T and dS^T -> TMEM (A operands of the dV / dK TS-MMAs); dS^T also -> smem (B of dQ^T)
+      tmem_st32(tmem + lane_off + 128, pp);
+      tmem_st32(tmem + lane_off + 160, pd);
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
         const uint32_t off = sw128_offset(r, ch);
-        *reinterpret_cast<uint4*>(sP + off) = make_uint4(pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]);
         *reinterpret_cast<uint4*>(sDS + off) = make_uint4(pd[4 * ch], pd[4 * ch + 1], pd[4 * ch + 2], pd[4 * ch + 3]);
       }
+      tmem_wait_st();
+      tc_fence_before();
       fence_async_smem();
       mbar_arrive(&bar.pds_full);
     }
@@ -375,33 +376,26 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     QIter it;
     it.begin(p.cu, p.tq, s0, s1, tok_first);
     for (int i = 0; it.valid(); it.next(), ++i) {
-      const int b = i & 1;
-      mbar_wait(&bar.dq_full[b], (i >> 1) & 1);
+      mbar_wait(&bar.dq_full, i & 1);
       tc_fence_after();
       uint32_t u[64];
-      tmem_ld32(tmem + lane_off + 128 + b * 64, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
-      tmem_ld32(tmem + lane_off + 128 + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
+      tmem_ld32(tmem + lane_off + 192, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
+      tmem_ld32(tmem + lane_off + 192 + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
       tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(&bar.dq_empty[b]);
-      // transpose through smem ([row][64 d] fp32, one half of d at a time) and reduce-add each
-      // half into dq_acc with one TMA bulk tensor reduce
+      mbar_arrive(&bar.dq_empty);
+      // transpose through smem ([row][d] fp32) and reduce-add the tile into dq_acc with one
+      // TMA bulk tensor reduce
       float* stg = reinterpret_cast<float*>(base + kOffStage);
-      const int row0 = p.cu[it.s] + it.tok;
-#pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        if (threadIdx.x == 128) bulk_wait_read<0>();  // the previous reduce has read the staging tile
-        named_bar_sync(1, 128);
-        if ((d >> 6) == half) {
+      if (threadIdx.x == 128) bulk_wait_read<0>();  // the previous tile's reduce has read the staging
+      named_bar_sync(1, 128);
 #pragma unroll
-          for (int c = 0; c < kBQ; ++c) stg[c * 64 + (d & 63)] = __uint_as_float(u[c]);
-          fence_async_smem();
-        }
-        named_bar_sync(1, 128);
-        if (threadIdx.x == 128) {
-          tma_reduce_add_3d(&p.tm_dq, stg, half * 64, hk * G, row0);
-          bulk_commit();
-        }
+      for (int c = 0; c < kBQ; ++c) stg[c * D + d] = __uint_as_float(u[c]);
+      fence_async_smem();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == 128) {
+        tma_reduce_add_3d(&p.tm_dq, stg, 0, hk * G, p.cu[it.s] + it.tok);
+        bulk_commit();
       }
     }
     if (threadIdx.x == 128) bulk_wait<0>();
@@ -490,7 +484,7 @@ int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const __nv_bfloat16* xsplit,
       return DKV_ERR_CUDA;
     }
   }
-  if (!make_map_3d_f32(&p.tm_dq, dq_acc, a.total_q, a.heads, D, G, tq, 64)) {
+  if (!make_map_3d_f32(&p.tm_dq, dq_acc, a.total_q, a.heads, D, G, tq, D)) {
     set_error("cuTensorMapEncodeTiled failed (backward dq_acc)");
     return DKV_ERR_CUDA;
   }
