@@ -33,10 +33,31 @@ DKV_DEVICE void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// per-warpgroup register budget (all 4 warps of an aligned warpgroup must execute it)
+template <int N>
+DKV_DEVICE void regs_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+DKV_DEVICE void regs_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 DKV_DEVICE float ex2(float x) {
   float y;
   asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA/ALU pipes (no MUFU): round-to-nearest split x = n + f, f in [-1/2, 1/2],
+// degree-3 relative-minimax polynomial for 2^f (max rel err 7.5e-5, below bf16 resolution of
+// the P operand), exponent added as an integer.  x is clamped to >= -125 (result ~2^-125, not 0).
+DKV_DEVICE float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: round(x) lands in the low mantissa bits
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05517025f, f, 0.24260791f), f, 0.69326091f), f, 0.99992830f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
 DKV_DEVICE uint32_t pack_bf16(float lo, float hi) {

@@ -253,9 +253,17 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
           for (int c = 0; c < kBN; ++c)
             if (c > lim) s[c] = -INFINITY;
         }
-        float mx = s[0];
+        // row max: 8 independent chains + a 3-level tree (a single 128-long dependent chain
+        // of FMNMX would sit on the softmax critical path)
+        float m8[8];
 #pragma unroll
-        for (int c = 1; c < kBN; ++c) mx = fmaxf(mx, s[c]);
+        for (int i = 0; i < 8; ++i) m8[i] = s[i];
+#pragma unroll
+        for (int c = 8; c < kBN; c += 8)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) m8[i] = fmaxf(m8[i], s[c + i]);
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
         const float m_tile = mx * p.scale_log2;
         const float m_new = fmaxf(m_run, m_tile);
         float alpha = 1.f;
@@ -264,19 +272,23 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
           m_run = m_new;
         }
         const float m_use = m_run == -INFINITY ? 0.f : m_run;
-        float rowsum = 0.f;
+        float rs[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c0 = 0; c0 < kBN; c0 += 32) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float e0 = ex2(fmaf(s[c0 + 2 * i], p.scale_log2, -m_use));
-            const float e1 = ex2(fmaf(s[c0 + 2 * i + 1], p.scale_log2, -m_use));
-            rowsum += e0 + e1;
+            const float x0 = fmaf(s[c0 + 2 * i], p.scale_log2, -m_use);
+            const float x1 = fmaf(s[c0 + 2 * i + 1], p.scale_log2, -m_use);
+            // 1 in 4 exponentials on the FMA pipe (polynomial) to unload the MUFU pipe
+            const float e0 = i >= 12 ? ex2_poly(x0) : ex2(x0);
+            const float e1 = i >= 12 ? ex2_poly(x1) : ex2(x1);
+            rs[i & 3] += e0 + e1;
             pk[i] = pack_bf16(e0, e1);
           }
           tmem_st16(tS + c0 / 2, pk);
         }
+        const float rowsum = (rs[0] + rs[1]) + (rs[2] + rs[3]);
         l_run = l_run * alpha + rowsum;
         // O holds P V of iterations < it (its MMA completed before S(it) did)
         if (it > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
