@@ -220,11 +220,16 @@ def main():
     dec = dkv.DualKVInput(q, kc, vc, kd, vd, cu)
 
     def step():
+        # Call 1 + Call 2 fused: one forward launch, one backward launch (prompt grads cast once)
+        oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc, dec)
+        return dkv.dualkv_two_call_bwd(qc, dec, oc, lc, doc, od, ld, dod, deterministic=False)
+
+    def step_separate():
+        # the reference's two separate calls (layer.py:243-255, 274-275), for comparison
         oc, lc = dkv.fa2_varlen_fwd(ctx_b)
         od, ld = dkv.dualkv_fwd(dec)
-        gd = dkv.dualkv_bwd(dec, od, ld, dod, deterministic=False)
-        gc = dkv.fa2_varlen_bwd(ctx_b, oc, lc, doc)
-        return oc, od, gd, gc
+        dkv.dualkv_bwd(dec, od, ld, dod, deterministic=False)
+        dkv.fa2_varlen_bwd(ctx_b, oc, lc, doc)
 
     def barrier():
         if world > 1:
@@ -262,16 +267,16 @@ def main():
     saved = {}
 
     def fwd_only():
-        saved["oc"], saved["lc"] = dkv.fa2_varlen_fwd(ctx_b)
-        saved["od"], saved["ld"] = dkv.dualkv_fwd(dec)
+        saved["oc"], saved["lc"], saved["od"], saved["ld"] = dkv.dualkv_two_call_fwd(qc, dec)
 
     fwd_ms = timed(fwd_only, args.steps)
 
     def bwd_only():
-        dkv.dualkv_bwd(dec, saved["od"], saved["ld"], dod, deterministic=False)
-        dkv.fa2_varlen_bwd(ctx_b, saved["oc"], saved["lc"], doc)
+        dkv.dualkv_two_call_bwd(qc, dec, saved["oc"], saved["lc"], doc, saved["od"], saved["ld"], dod,
+                                deterministic=False)
 
     bwd_ms = timed(bwd_only, args.steps)
+    sep_ms = timed(step_separate, args.steps)
     fl_step = flops_fwdbwd(c)
     value = fl_step * world / (ms * 1e-3) / 1e12
 
@@ -299,21 +304,19 @@ def main():
         host_in = {k: v.cpu().pin_memory() for k, v in
                    dict(qc=qc, kc=kc, vc=vc, q=q, kd=kd, vd=vd, doc=doc, dod=dod).items()}
         out_shapes = [(p, h, d), (t, h, d), (t, h, d), (p, hk, d), (p, hk, d), (t, hk, d), (t, hk, d),
-                      (p, h, d), (p, hk, d), (p, hk, d)]
+                      (p, h, d)]
         host_out = [torch.empty(s_, dtype=torch.bfloat16).pin_memory() for s_ in out_shapes]
         h2d = sum(x.numel() * x.element_size() for x in host_in.values())
         d2h = sum(x.numel() * x.element_size() for x in host_out)
 
         def e2e_step():
             dv_ = {k: v.to(dev, non_blocking=True) for k, v in host_in.items()}
-            cb = dkv.VarlenBatch(dv_["qc"], dv_["kc"], dv_["vc"], cuc)
             di = dkv.DualKVInput(dv_["q"], dv_["kc"], dv_["vc"], dv_["kd"], dv_["vd"], cu)
-            oc, lc = dkv.fa2_varlen_fwd(cb)
-            od, ld = dkv.dualkv_fwd(di)
-            gq, gkc, gvc, gkd, gvd = dkv.dualkv_bwd(di, od, ld, dv_["dod"], deterministic=False)
-            cq, ck, cv = dkv.fa2_varlen_bwd(cb, oc, lc, dv_["doc"])
-            # total prompt KV gradient = Call 1 + Call 2 contributions (layer.py:278-279)
-            outs = [oc, od, gq, gkc + ck, gvc + cv, gkd, gvd, cq, ck, cv]
+            oc, lc, od, ld = dkv.dualkv_two_call_fwd(dv_["qc"], di)
+            cq, gkc, gvc, gq, gkd, gvd = dkv.dualkv_two_call_bwd(dv_["qc"], di, oc, lc, dv_["doc"], od, ld,
+                                                                 dv_["dod"], deterministic=False)
+            # every output of the layer's attention: both O's and all six input gradients
+            outs = [oc, od, gq, gkc, gvc, gkd, gvd, cq]
             for ho, o in zip(host_out, outs):
                 ho.copy_(o, non_blocking=True)
 
@@ -331,16 +334,16 @@ def main():
     except Exception:
         pass
     peak_burst = peaks.get("bf16_tflops", 1590.0)
-    # per step the main kernels launch twice (Call 2 and Call 1); achieved = their total
-    # algorithmic FLOPs / their total device time (CUDA events around each launch)
-    launches_per_step = 2
+    # per step each main kernel launches once (Call 1 fused into the Call 2 launch); achieved =
+    # algorithmic FLOPs / device time of that launch (CUDA events recorded around it by libdkv)
+    launches_per_step = 1
     bwd_kernel_ms = bms.value / max(1, bl.value)
     fwd_kernel_ms = fms.value / max(1, fl.value)
     bwd_flops_per_launch = 10 * pairs(p, [r] * n) * h * d / launches_per_step
     fwd_flops_per_launch = 4 * pairs(p, [r] * n) * h * d / launches_per_step
     bwd_ach = bwd_flops_per_launch / (bwd_kernel_ms * 1e-3) / 1e12
     fwd_ach = fwd_flops_per_launch / (fwd_kernel_ms * 1e-3) / 1e12
-    roof = {"bound": "tensor", "kernel": "dualkv_bwd_kernel (tcgen05, Call 1 + Call 2 launches averaged)",
+    roof = {"bound": "tensor", "kernel": "dualkv_bwd_kernel (tcgen05; Call 1 fused into the Call 2 launch)",
             "achieved": round(bwd_ach, 2), "peak": peak_burst, "unit": "TFLOP/s",
             "frac": round(bwd_ach / peak_burst, 4), "traffic": None,
             "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "fallback 1.59 PF",
@@ -365,9 +368,10 @@ def main():
                        "N": n, "P": p, "R": r, "H": h, "H_k": hk, "d": d,
                        "global_groups": world, "parallelism": f"dp{world} over prompt groups",
                        "l2": "inputs larger than L2 (q alone 512 MiB > 126 MB)",
-                       "unit_of_work": "Call1+Call2 fwd+bwd (reference run_bench dk unit)",
+                       "unit_of_work": "Call1+Call2 fwd+bwd (reference run_bench dk unit), fused two-call launches",
                        "flops_per_group": fl_step},
             "fwd_ms": round(fwd_ms, 3), "bwd_ms": round(bwd_ms, 3),
+            "separate_calls_ms_per_step": round(sep_ms, 3),
             "fwd_tflops": round(4 * pairs(p, [r] * n) * h * d / (fwd_ms * 1e-3) / 1e12, 2),
             "bwd_tflops": round(10 * pairs(p, [r] * n) * h * d / (bwd_ms * 1e-3) / 1e12, 2),
             "replicated_ncopy": rep, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,

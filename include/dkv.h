@@ -111,6 +111,32 @@ DKV_API int64_t dkv_bwd_num_ctx_chunks(const dkv_bwd_params* p);
 DKV_API int32_t dkv_dualkv_bwd(const dkv_bwd_params* p, void* workspace, size_t workspace_bytes, void* stream);
 DKV_API int32_t dkv_varlen_bwd(const dkv_bwd_params* p, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Fused two-call launch (layer.py:236-290, §3): Call 1 -- causal self-attention of
+ * the prompt's own queries over the single prompt copy -- runs inside the Call 2 launch (its
+ * work items fill the tail).  In the backward both calls accumulate the prompt-key gradient in
+ * ONE fp32 scratch, cast once into call2.dk_ctx / call2.dv_ctx (the TOTAL prompt gradient;
+ * the reference instead adds two separately cast contributions, layer.py:278-279). */
+typedef struct dkv_twocall_fwd_params {
+  dkv_fwd_params call2; /* the two-region problem; call2.k_ctx / v_ctx are the prompt's keys */
+  const void* q_ctx;    /* [ctx_len, heads, head_dim] the prompt's own queries */
+  void* out_ctx;        /* [ctx_len, heads, head_dim] */
+  float* lse_ctx;       /* [heads, ctx_len] */
+} dkv_twocall_fwd_params;
+
+typedef struct dkv_twocall_bwd_params {
+  dkv_bwd_params call2; /* ctx_partials must be NULL */
+  const void* q_ctx;
+  const void* out_ctx;
+  const float* lse_ctx;
+  const void* dout_ctx;
+  void* dq_ctx;         /* [ctx_len, heads, head_dim] */
+} dkv_twocall_bwd_params;
+
+DKV_API int32_t dkv_twocall_fwd(const dkv_twocall_fwd_params* p, void* stream);
+DKV_API size_t dkv_twocall_bwd_workspace_size(const dkv_twocall_bwd_params* p);
+DKV_API int32_t dkv_twocall_bwd(const dkv_twocall_bwd_params* p, void* workspace, size_t workspace_bytes,
+                                void* stream);
+
 /* dst[i] = RNE_bf16(src[i]), bit-identical to the reference bf16_round. */
 DKV_API int32_t dkv_convert_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
 

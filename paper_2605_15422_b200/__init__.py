@@ -15,6 +15,9 @@ from .api import (  # noqa: F401
     dualkv_attention_varlen,
     dualkv_bwd,
     dualkv_fwd,
+    dualkv_two_call_attention,
+    dualkv_two_call_bwd,
+    dualkv_two_call_fwd,
     fa2_varlen_bwd,
     fa2_varlen_fwd,
     uses_tensor_cores,

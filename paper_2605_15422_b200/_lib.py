@@ -43,6 +43,15 @@ class BwdParams(ctypes.Structure):
     ]
 
 
+class TwoCallFwdParams(ctypes.Structure):
+    _fields_ = [("call2", FwdParams), ("q_ctx", _vp), ("out_ctx", _vp), ("lse_ctx", _vp)]
+
+
+class TwoCallBwdParams(ctypes.Structure):
+    _fields_ = [("call2", BwdParams), ("q_ctx", _vp), ("out_ctx", _vp), ("lse_ctx", _vp),
+                ("dout_ctx", _vp), ("dq_ctx", _vp)]
+
+
 # every symbol include/dkv.h declares, with its ctypes signature
 SIGNATURES = {
     "dkv_abi_version": (ctypes.c_int32, []),
@@ -54,6 +63,9 @@ SIGNATURES = {
     "dkv_bwd_num_ctx_chunks": (_i64, [ctypes.POINTER(BwdParams)]),
     "dkv_dualkv_bwd": (ctypes.c_int32, [ctypes.POINTER(BwdParams), _vp, ctypes.c_size_t, _vp]),
     "dkv_varlen_bwd": (ctypes.c_int32, [ctypes.POINTER(BwdParams), _vp, ctypes.c_size_t, _vp]),
+    "dkv_twocall_fwd": (ctypes.c_int32, [ctypes.POINTER(TwoCallFwdParams), _vp]),
+    "dkv_twocall_bwd_workspace_size": (ctypes.c_size_t, [ctypes.POINTER(TwoCallBwdParams)]),
+    "dkv_twocall_bwd": (ctypes.c_int32, [ctypes.POINTER(TwoCallBwdParams), _vp, ctypes.c_size_t, _vp]),
     "dkv_convert_f32_to_bf16": (ctypes.c_int32, [_vp, _vp, _i64, _vp]),
     "dkv_gather_rows": (ctypes.c_int32, [_vp, _vp, _i64, _vp, _i64, _vp]),
     "dkv_segment_sum_rows": (ctypes.c_int32, [_vp, _vp, ctypes.c_int32, _i64, _vp, _vp, _i64, _vp]),

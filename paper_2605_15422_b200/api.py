@@ -25,13 +25,13 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import BwdParams, FwdParams, check, lib
+from ._lib import BwdParams, FwdParams, TwoCallBwdParams, TwoCallFwdParams, check, lib
 
 __all__ = [
     "DualKVInput", "VarlenBatch", "ContextGradScratch",
     "dualkv_fwd", "dualkv_bwd", "context_grad_contributions", "convert_dkv_context",
     "bf16_naive_accumulate", "fa2_varlen_fwd", "fa2_varlen_bwd", "dualkv_attention_varlen",
-    "uses_tensor_cores",
+    "uses_tensor_cores", "dualkv_two_call_fwd", "dualkv_two_call_bwd", "dualkv_two_call_attention",
 ]
 
 _DTYPES = {torch.bfloat16: _lib.DKV_BF16, torch.float32: _lib.DKV_F32}
@@ -232,25 +232,24 @@ def ctypes_ref(s):
 # backward (kernel.py:213-305, fa2.py:268-306)
 # ---------------------------------------------------------------------------
 
-def _bwd_run(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse, d_out, deterministic,
-             ctx_chunk=0, partials_for_chunks=False, varlen=False):
+def _bwd_params(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse, d_out, deterministic,
+                ctx_chunk=0):
+    """Shape checks, output allocation and the C parameter block of one backward."""
     t, h, d = q.shape
     if tuple(d_out.shape) != tuple(q.shape) or tuple(out.shape) != tuple(q.shape):
         raise ValueError(f"O/dO shape {tuple(out.shape)}/{tuple(d_out.shape)} inconsistent with q "
                          f"{tuple(q.shape)}")
     if tuple(lse.shape) != (h, t):
         raise ValueError(f"lse shape {tuple(lse.shape)} != {(h, t)}")
-    out = out.to(q.dtype).contiguous()
-    d_out = d_out.to(q.dtype).contiguous()
-    lse = lse.to(torch.float32).contiguous()
-    dq = torch.empty_like(q)
-    dk = torch.empty_like(k)
-    dv = torch.empty_like(v)
+    keep = dict(out=out.to(q.dtype).contiguous(), d_out=d_out.to(q.dtype).contiguous(),
+                lse=lse.to(torch.float32).contiguous())
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     dkc = torch.empty_like(kc) if kc is not None else None
     dvc = torch.empty_like(vc) if vc is not None else None
     prm = BwdParams()
     prm.q, prm.k_ctx, prm.v_ctx, prm.k, prm.v = _ptr(q), _ptr(kc), _ptr(vc), _ptr(k), _ptr(v)
-    prm.cu_seqlens, prm.out, prm.lse, prm.dout = cu_dev.data_ptr(), _ptr(out), _ptr(lse), _ptr(d_out)
+    prm.cu_seqlens, prm.out = cu_dev.data_ptr(), _ptr(keep["out"])
+    prm.lse, prm.dout = _ptr(keep["lse"]), _ptr(keep["d_out"])
     prm.dq, prm.dk_ctx, prm.dv_ctx, prm.dk, prm.dv = _ptr(dq), _ptr(dkc), _ptr(dvc), _ptr(dk), _ptr(dv)
     prm.num_seqs, prm.total_q, prm.ctx_len = n, t, p_len
     prm.heads, prm.kv_heads, prm.head_dim = h, k.shape[1], d
@@ -259,18 +258,26 @@ def _bwd_run(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse, d_out
     prm.dtype = _DTYPES[q.dtype]
     prm.deterministic = 1 if deterministic else 0
     prm.ctx_chunk = int(ctx_chunk)
+    return prm, (dq, dkc, dvc, dk, dv), keep
+
+
+def _bwd_run(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse, d_out, deterministic,
+             ctx_chunk=0, partials_for_chunks=False, varlen=False):
+    prm, grads, keep = _bwd_params(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse, d_out,
+                                   deterministic, ctx_chunk)
     partials = None
     if partials_for_chunks:
         nch = int(lib.dkv_bwd_num_ctx_chunks(ctypes_ref(prm)))
         kk = kc if kc is not None else k
-        partials = torch.empty((nch, 2, p_len, kk.shape[1], d), dtype=torch.float32, device=q.device)
+        partials = torch.empty((nch, 2, p_len, kk.shape[1], q.shape[2]), dtype=torch.float32, device=q.device)
         prm.ctx_partials = _ptr(partials)
     ws_bytes = int(lib.dkv_bwd_workspace_size(ctypes_ref(prm)))
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)
     fn = lib.dkv_varlen_bwd if varlen else lib.dkv_dualkv_bwd
     check(fn(ctypes_ref(prm), ws.data_ptr(), ws_bytes, _stream()),
           "fa2_varlen_bwd" if varlen else "dualkv_bwd")
-    return dq, dkc, dvc, dk, dv, partials
+    del keep
+    return grads + (partials,)
 
 
 def dualkv_bwd(inp: DualKVInput, out, lse, d_out, deterministic: bool = True,
@@ -393,3 +400,97 @@ def dualkv_attention_varlen(q, k_context, v_context, k_decoded, v_decoded, cu_se
                       softmax_scale=softmax_scale, causal=causal, tile_size=tile_size)
     return _DualKVFunction.apply(inp.q, inp.k_context, inp.v_context, inp.k_decoded,
                                  inp.v_decoded, inp)
+
+
+# ---------------------------------------------------------------------------
+# fused two-call op (layer.py:236-290 composed in one launch)
+# ---------------------------------------------------------------------------
+
+def _check_prompt_q(q_ctx, inp: DualKVInput):
+    q_ctx = _check_tensor(q_ctx, "q_context")
+    p_len = inp.context_seqlen
+    if tuple(q_ctx.shape) != (p_len, inp.q.shape[1], inp.q.shape[2]) or q_ctx.dtype != inp.q.dtype:
+        raise ValueError(f"q_context shape/dtype {tuple(q_ctx.shape)}/{q_ctx.dtype} inconsistent with "
+                         f"P={p_len}, q {tuple(inp.q.shape)}/{inp.q.dtype}")
+    return q_ctx
+
+
+def dualkv_two_call_fwd(q_context, inp: DualKVInput):
+    """Call 1 (causal self-attention of the prompt's own queries) + Call 2 (DualKV) in ONE launch.
+
+    Returns (O_ctx [P,H,d], lse_ctx [H,P], O_dec [sum R_i,H,d], lse_dec [H,sum R_i]) -- equal to
+    `fa2_varlen_fwd` over the prompt and `dualkv_fwd(inp)` (layer.py:243-255)."""
+    q_ctx = _check_prompt_q(q_context, inp)
+    q = inp.q
+    p_len, h, d = q_ctx.shape
+    out = torch.empty_like(q)
+    lse = torch.empty((h, q.shape[0]), dtype=torch.float32, device=q.device)
+    out_c = torch.empty_like(q_ctx)
+    lse_c = torch.empty((h, p_len), dtype=torch.float32, device=q.device)
+    prm = TwoCallFwdParams()
+    prm.call2 = _fwd_params(q, inp.k_context, inp.v_context, inp.k_decoded, inp.v_decoded, inp.cu_dev,
+                            inp.num_sequences, p_len, inp._grid_max, inp.softmax_scale, out, lse)
+    prm.q_ctx, prm.out_ctx, prm.lse_ctx = _ptr(q_ctx), _ptr(out_c), _ptr(lse_c)
+    check(lib.dkv_twocall_fwd(ctypes_ref(prm), _stream()), "dualkv_two_call_fwd")
+    return out_c, lse_c, out, lse
+
+
+def dualkv_two_call_bwd(q_context, inp: DualKVInput, out_ctx, lse_ctx, d_out_ctx, out, lse, d_out,
+                        deterministic: bool = True):
+    """Backward of both calls in ONE launch.  Returns (dQ_ctx, dK_c, dV_c, dQ_dec, dK_dec, dV_dec),
+    dK_c / dV_c being the TOTAL prompt-key gradient (Call 1 + Call 2, layer.py:278-279) accumulated
+    in one fp32 scratch and cast once."""
+    q_ctx = _check_prompt_q(q_context, inp)
+    p_len, h, d = q_ctx.shape
+    if tuple(out_ctx.shape) != tuple(q_ctx.shape) or tuple(d_out_ctx.shape) != tuple(q_ctx.shape):
+        raise ValueError("O_ctx/dO_ctx shape inconsistent with q_context")
+    if tuple(lse_ctx.shape) != (h, p_len):
+        raise ValueError(f"lse_ctx shape {tuple(lse_ctx.shape)} != {(h, p_len)}")
+    prm2, grads, keep = _bwd_params(inp.q, inp.k_context, inp.v_context, inp.k_decoded, inp.v_decoded,
+                                    inp.cu_dev, inp.num_sequences, p_len, inp._grid_max, inp.softmax_scale,
+                                    out, lse, d_out, deterministic)
+    dq, dkc, dvc, dkd, dvd = grads
+    o_c = out_ctx.to(q_ctx.dtype).contiguous()
+    l_c = lse_ctx.to(torch.float32).contiguous()
+    do_c = d_out_ctx.to(q_ctx.dtype).contiguous()
+    dq_c = torch.empty_like(q_ctx)
+    prm = TwoCallBwdParams()
+    prm.call2 = prm2
+    prm.q_ctx, prm.out_ctx, prm.lse_ctx = _ptr(q_ctx), _ptr(o_c), _ptr(l_c)
+    prm.dout_ctx, prm.dq_ctx = _ptr(do_c), _ptr(dq_c)
+    ws_bytes = int(lib.dkv_twocall_bwd_workspace_size(ctypes_ref(prm)))
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q_ctx.device)
+    check(lib.dkv_twocall_bwd(ctypes_ref(prm), ws.data_ptr(), ws_bytes, _stream()), "dualkv_two_call_bwd")
+    del keep
+    return dq_c, dkc, dvc, dq, dkd, dvd
+
+
+class _TwoCallFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q_context, k_context, v_context, q, k_decoded, v_decoded, inp):
+        o_c, l_c, o, l = dualkv_two_call_fwd(q_context, inp)
+        ctx.save_for_backward(q_context, o_c, l_c, o, l)
+        ctx.inp = inp
+        return o_c, o
+
+    @staticmethod
+    def backward(ctx, d_oc, d_o):
+        q_c, o_c, l_c, o, l = ctx.saved_tensors
+        d_oc = torch.zeros_like(o_c) if d_oc is None else d_oc.contiguous()
+        d_o = torch.zeros_like(o) if d_o is None else d_o.contiguous()
+        dq_c, dkc, dvc, dq, dkd, dvd = dualkv_two_call_bwd(q_c, ctx.inp, o_c, l_c, d_oc, o, l, d_o,
+                                                           deterministic=False)
+        return dq_c, dkc, dvc, dq, dkd, dvd, None
+
+
+def dualkv_two_call_attention(q_context, k_context, v_context, q_decoded, k_decoded, v_decoded,
+                              cu_seqlens_q, max_seqlen_q: Optional[int] = None,
+                              softmax_scale: Optional[float] = None):
+    """The whole attention of one prompt group in the P+NR layout (layer.py:236-290): returns
+    (O_context [P,H,d], O_decoded [sum R_i,H,d]); autograd gives all six input gradients, the
+    prompt K/V gradient summed over both calls and all N sequences in fp32 and cast once."""
+    inp = DualKVInput(q_decoded, k_context, v_context, k_decoded, v_decoded, cu_seqlens_q,
+                      max_seqlen_q=max_seqlen_q, softmax_scale=softmax_scale)
+    q_ctx = _check_prompt_q(q_context, inp)
+    return _TwoCallFunction.apply(q_ctx, inp.k_context, inp.v_context, inp.q, inp.k_decoded,
+                                  inp.v_decoded, inp)

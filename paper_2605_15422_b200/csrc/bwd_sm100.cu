@@ -63,6 +63,10 @@ static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory per
 struct Params {
   CUtensorMap tm_q, tm_do, tm_k, tm_v, tm_kc, tm_vc, tm_dq;
   CUtensorMap tm_x;     // xsplit [Hk*tpad*G rows][32] bf16: split3(-lse/scale) | split3(-D)
+  // fused Call 1 (two-call launch): the prompt's own queries, their (lse, D) rows and dQ
+  CUtensorMap tm_qs, tm_dos, tm_xs, tm_dqs;
+  int cu_self[2];       // {0, P}: the prompt as a one-sequence "cu_seqlens"
+  int tpad_s, n_self_items, self_part;
   float* dq_acc;        // [T][H][D] f32
   __nv_bfloat16* dk;    // [T][Hk][D]
   __nv_bfloat16* dv;
@@ -121,12 +125,15 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars& bar = *reinterpret_cast<Bars*>(base + kOffBar);
 
-  // ---- decode the work item
+  // ---- decode the work item (grid order = longest first: kinds 0, 2, 1).
+  // kind 0: shared-prompt key tile x chunk of sequences (Call 2);
+  // kind 1: own-response key tile of one sequence (Call 2); kind 2 (two-call launch only):
+  // prompt key tile x the prompt's own causal queries (Call 1), accumulated into the same fp32
+  // shared-prompt scratch so the total prompt gradient is cast once.
   const int bid = blockIdx.x;
-  bool is_ctx;
-  int hk, ktile, s0, s1, tok_first, kv_len, kv_row0;
+  int kind, hk, ktile, s0, s1, tok_first, kv_len, kv_row0, part = 0;
   if (bid < p.n_ctx_items) {
-    is_ctx = true;
+    kind = 0;
     const int per_chunk = p.n_ctx_tiles * p.kv_heads;
     const int chunk_id = bid / per_chunk;
     const int rem = bid % per_chunk;
@@ -137,9 +144,10 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     tok_first = 0;
     kv_len = p.ctx_len;
     kv_row0 = 0;
-  } else {
-    is_ctx = false;
-    const int b2 = bid - p.n_ctx_items;
+    part = p.atomic_ctx ? 0 : chunk_id;
+  } else if (bid >= p.n_ctx_items + p.n_self_items) {
+    kind = 1;
+    const int b2 = bid - p.n_ctx_items - p.n_self_items;
     hk = b2 % p.kv_heads;
     const int r2 = b2 / p.kv_heads;
     s0 = r2 % p.num_seqs;
@@ -149,12 +157,31 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     if (ktile * kBK >= kv_len) return;
     tok_first = (ktile * kBK / p.tq) * p.tq;
     kv_row0 = p.cu[s0];
+  } else {
+    kind = 2;
+    const int b3 = bid - p.n_ctx_items;
+    hk = b3 % p.kv_heads;
+    ktile = b3 / p.kv_heads;
+    s0 = 0;
+    s1 = 1;
+    kv_len = p.ctx_len;
+    tok_first = (ktile * kBK / p.tq) * p.tq;
+    kv_row0 = 0;
+    part = p.atomic_ctx ? 0 : p.self_part;
   }
+  const bool ctx_keys = kind != 1;  // keys are the shared prompt copy (output -> fp32 scratch)
+  const bool causal = kind != 0;
+  const int32_t* cu = kind == 2 ? p.cu_self : p.cu;
+  const CUtensorMap* mq = kind == 2 ? &p.tm_qs : &p.tm_q;
+  const CUtensorMap* mdo = kind == 2 ? &p.tm_dos : &p.tm_do;
+  const CUtensorMap* mx = kind == 2 ? &p.tm_xs : &p.tm_x;
+  const CUtensorMap* mdq = kind == 2 ? &p.tm_dqs : &p.tm_dq;
+  const int xtpad = kind == 2 ? p.tpad_s : p.tpad;
   const int kbase = ktile * kBK;  // region-local first key of the tile
   int nq = 0;
   {
     QIter it;
-    it.begin(p.cu, p.tq, s0, s1, tok_first);
+    it.begin(cu, p.tq, s0, s1, tok_first);
     for (; it.valid(); it.next()) ++nq;
   }
   if (nq == 0) return;  // context chunk of empty responses: scratch already zero
@@ -200,13 +227,13 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
 
   if (warp == 8) {
     // ================= producer: K/V once, then (Q, dO, lse/D) per query tile
-    const CUtensorMap* mk = is_ctx ? &p.tm_kc : &p.tm_k;
-    const CUtensorMap* mv = is_ctx ? &p.tm_vc : &p.tm_v;
+    const CUtensorMap* mk = ctx_keys ? &p.tm_kc : &p.tm_k;
+    const CUtensorMap* mv = ctx_keys ? &p.tm_vc : &p.tm_v;
     if (lane == 0) {
-      tma_prefetch(&p.tm_q);
-      tma_prefetch(&p.tm_do);
-      tma_prefetch(&p.tm_dq);
-      tma_prefetch(&p.tm_x);
+      tma_prefetch(mq);
+      tma_prefetch(mdo);
+      tma_prefetch(mdq);
+      tma_prefetch(mx);
       tma_prefetch(mk);
       tma_prefetch(mv);
       mbar_arrive_expect_tx(&bar.kv_full, 2 * kKVBytes);
@@ -218,23 +245,23 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     const uint64_t pol_q = policy_evict_last();
     if (lane == 0) {
       QIter it;
-      it.begin(p.cu, p.tq, s0, s1, tok_first);
+      it.begin(cu, p.tq, s0, s1, tok_first);
       for (int i = 0; it.valid(); it.next(), ++i) {
         const int st = i % kStages;
         const uint32_t ph = (i / kStages) & 1;
         mbar_wait(&bar.q_empty[st], ph ^ 1);
-        const int row0 = p.cu[it.s] + it.tok;
+        const int row0 = cu[it.s] + it.tok;
         mbar_arrive_expect_tx(&bar.q_full[st], 2 * kQBytes + 2 * kXBytes);
         for (int pn = 0; pn < 2; ++pn) {
-          tma_load_3d_hint(base + kOffQ + st * kQBytes + pn * kQPanel, &p.tm_q, &bar.q_full[st], pn * 64,
+          tma_load_3d_hint(base + kOffQ + st * kQBytes + pn * kQPanel, mq, &bar.q_full[st], pn * 64,
                            hk * G, row0, pol_q);
-          tma_load_3d_hint(base + kOffDO + st * kQBytes + pn * kQPanel, &p.tm_do, &bar.q_full[st], pn * 64,
+          tma_load_3d_hint(base + kOffDO + st * kQBytes + pn * kQPanel, mdo, &bar.q_full[st], pn * 64,
                            hk * G, row0, pol_q);
         }
         // the tile's 64 additive-constant rows: -lse/scale (cols 0-15) and -D (cols 16-31)
-        const int xrow = (hk * p.tpad + row0) * G;
-        tma_load_2d(base + kOffX + st * 2 * kXBytes, &p.tm_x, &bar.q_full[st], 0, xrow);
-        tma_load_2d(base + kOffX + st * 2 * kXBytes + kXBytes, &p.tm_x, &bar.q_full[st], 16, xrow);
+        const int xrow = (hk * xtpad + row0) * G;
+        tma_load_2d(base + kOffX + st * 2 * kXBytes, mx, &bar.q_full[st], 0, xrow);
+        tma_load_2d(base + kOffX + st * 2 * kXBytes + kXBytes, mx, &bar.q_full[st], 16, xrow);
       }
     }
   } else if (warp == 9) {
@@ -308,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     const int key = kbase + r;  // region-local key index
     uint8_t* sDS = base + kOffDS;
     QIter it;
-    it.begin(p.cu, p.tq, s0, s1, tok_first);
+    it.begin(cu, p.tq, s0, s1, tok_first);
     for (int i = 0; it.valid(); it.next(), ++i) {
       const int st = i % kStages;
       mbar_wait(&bar.q_full[st], (i / kStages) & 1);
@@ -327,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       // i.e. columns c >= (k - tok0) * G (rows are token-major); columns past the sequence end
       // are never visible
       int cmin;
-      if (is_ctx) {
+      if (!causal) {
         cmin = key < kv_len ? 0 : kBQ;
       } else {
         const int dt = key - it.tok;
@@ -380,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     const int d = (warp - 4) * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>((warp - 4) * 32) << 16;
     QIter it;
-    it.begin(p.cu, p.tq, s0, s1, tok_first);
+    it.begin(cu, p.tq, s0, s1, tok_first);
     for (int i = 0; it.valid(); it.next(), ++i) {
       mbar_wait(&bar.dq_full, i & 1);
       tc_fence_after();
@@ -400,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       fence_async_smem();
       named_bar_sync(1, 128);
       if (threadIdx.x == 128) {
-        tma_reduce_add_3d(&p.tm_dq, stg, 0, hk * G, p.cu[it.s] + it.tok);
+        tma_reduce_add_3d(mdq, stg, 0, hk * G, cu[it.s] + it.tok);
         bulk_commit();
       }
     }
@@ -426,10 +453,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       if (!ok) continue;
 #pragma unroll
       for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * osc);
-      if (is_ctx) {
+      if (ctx_keys) {
         const int64_t plane = static_cast<int64_t>(p.ctx_len) * p.kv_heads * D;
-        const int chunk_id = s0 / p.chunk;
-        float* dst = p.ctx_acc + (p.atomic_ctx ? 0 : static_cast<int64_t>(chunk_id) * 2 * plane) +
+        float* dst = p.ctx_acc + static_cast<int64_t>(part) * 2 * plane +
                      (do_k ? 0 : plane) + (static_cast<int64_t>(key) * p.kv_heads + hk) * D + c0;
         if (p.atomic_ctx) {
 #pragma unroll
@@ -470,17 +496,19 @@ bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads) {
   return G <= bwd::kBQ && (bwd::kBQ % G) == 0;
 }
 
-int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const __nv_bfloat16* xsplit, int tpad, float* ctx_acc, int chunk,
-                  int num_chunks, bool atomic_ctx, cudaStream_t st) {
+int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, cudaStream_t st) {
   using namespace bwd;
   Params p{};
   const int G = a.heads / a.kv_heads;
   const int tq = kBQ / G;
-  if (!make_map_3d_bf16(&p.tm_q, a.q, a.total_q, a.heads, D, G, tq) ||
-      !make_map_3d_bf16(&p.tm_do, a.dout, a.total_q, a.heads, D, G, tq) ||
-      !make_map_3d_bf16(&p.tm_k, a.k, a.total_q, a.kv_heads, D, 1, kBK) ||
-      !make_map_3d_bf16(&p.tm_v, a.v, a.total_q, a.kv_heads, D, 1, kBK)) {
-    set_error("cuTensorMapEncodeTiled failed (backward q/dO/k/v)");
+  if (a.total_q > 0 &&
+      (!make_map_3d_bf16(&p.tm_q, a.q, a.total_q, a.heads, D, G, tq) ||
+       !make_map_3d_bf16(&p.tm_do, a.dout, a.total_q, a.heads, D, G, tq) ||
+       !make_map_3d_bf16(&p.tm_k, a.k, a.total_q, a.kv_heads, D, 1, kBK) ||
+       !make_map_3d_bf16(&p.tm_v, a.v, a.total_q, a.kv_heads, D, 1, kBK) ||
+       !make_map_3d_f32(&p.tm_dq, w.dq_acc, a.total_q, a.heads, D, G, tq, D) ||
+       !make_map_2d_bf16_sw32(&p.tm_x, w.xsplit, static_cast<int64_t>(w.tpad) * a.heads, 32, 16, kBQ))) {
+    set_error("cuTensorMapEncodeTiled failed (backward q/dO/k/v/dq/x)");
     return DKV_ERR_CUDA;
   }
   if (a.ctx_len > 0) {
@@ -490,19 +518,23 @@ int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const __nv_bfloat16* xsplit,
       return DKV_ERR_CUDA;
     }
   }
-  if (!make_map_3d_f32(&p.tm_dq, dq_acc, a.total_q, a.heads, D, G, tq, D)) {
-    set_error("cuTensorMapEncodeTiled failed (backward dq_acc)");
+  const bool with_self = self && a.ctx_len > 0;
+  if (with_self &&
+      (!make_map_3d_bf16(&p.tm_qs, self->q, a.ctx_len, a.heads, D, G, tq) ||
+       !make_map_3d_bf16(&p.tm_dos, self->dout, a.ctx_len, a.heads, D, G, tq) ||
+       !make_map_3d_f32(&p.tm_dqs, w.dq_acc_s, a.ctx_len, a.heads, D, G, tq, D) ||
+       !make_map_2d_bf16_sw32(&p.tm_xs, w.xsplit_s, static_cast<int64_t>(w.tpad_s) * a.heads, 32, 16, kBQ))) {
+    set_error("cuTensorMapEncodeTiled failed (backward fused Call 1 maps)");
     return DKV_ERR_CUDA;
   }
-  if (!make_map_2d_bf16_sw32(&p.tm_x, xsplit, static_cast<int64_t>(tpad) * a.heads, 32, 16, kBQ)) {
-    set_error("cuTensorMapEncodeTiled failed (backward additive-constant rows)");
-    return DKV_ERR_CUDA;
-  }
-  p.tpad = tpad;
-  p.dq_acc = dq_acc;
+  p.tpad = w.tpad;
+  p.tpad_s = w.tpad_s;
+  p.cu_self[0] = 0;
+  p.cu_self[1] = a.ctx_len;
+  p.dq_acc = w.dq_acc;
   p.dk = static_cast<__nv_bfloat16*>(a.dk);
   p.dv = static_cast<__nv_bfloat16*>(a.dv);
-  p.ctx_acc = ctx_acc;
+  p.ctx_acc = w.ctx_acc;
   p.cu = a.cu;
   p.num_seqs = a.num_seqs;
   p.total_q = a.total_q;
@@ -511,14 +543,17 @@ int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const __nv_bfloat16* xsplit,
   p.kv_heads = a.kv_heads;
   p.group = G;
   p.tq = tq;
-  p.chunk = chunk;
+  p.chunk = w.chunk;
   p.n_ctx_tiles = (a.ctx_len + kBK - 1) / kBK;
-  p.n_ctx_items = p.n_ctx_tiles * a.kv_heads * num_chunks;
-  p.atomic_ctx = atomic_ctx ? 1 : 0;
+  p.n_ctx_items = a.total_q > 0 ? p.n_ctx_tiles * a.kv_heads * w.num_chunks : 0;
+  p.n_self_items = with_self ? p.n_ctx_tiles * a.kv_heads : 0;
+  p.self_part = w.self_part;
+  p.atomic_ctx = w.atomic_ctx ? 1 : 0;
   p.scale = a.scale;
   p.scale_log2 = a.scale * 1.4426950408889634f;
-  const int max_tiles = (a.max_seqlen + kBK - 1) / kBK;
-  const int64_t grid = static_cast<int64_t>(p.n_ctx_items) + static_cast<int64_t>(max_tiles) * a.num_seqs * a.kv_heads;
+  const int max_tiles = a.total_q > 0 ? (a.max_seqlen + kBK - 1) / kBK : 0;
+  const int64_t grid = static_cast<int64_t>(p.n_ctx_items) + p.n_self_items +
+                       static_cast<int64_t>(max_tiles) * a.num_seqs * a.kv_heads;
   if (grid == 0) return DKV_OK;
   if (grid > 0x7fffffff) {
     set_error("backward grid too large");

@@ -113,7 +113,7 @@ static int fwd_impl(const dkv_fwd_params* p, bool dualkv, void* stream, const ch
   if (a.total_q == 0) return DKV_OK;
   prof_main_begin(0, st);
   if (tc_supported(a.dtype, a.head_dim, a.heads, a.kv_heads)) {
-    rc = launch_tc_fwd(a, st);
+    rc = launch_tc_fwd(a, nullptr, st);
     if (rc) return rc;
   } else {
     launch_simt_fwd(a, st);
@@ -142,42 +142,58 @@ static int auto_chunk(const dkv_bwd_params* p) {
 static int dpack_tpad(size_t T) { return static_cast<int>((T + 3) & ~size_t(3)); }
 
 struct BwdLayout {
-  size_t drow, dpack, dq_acc, ctx, total;
-  int chunk, num_chunks, num_parts;
+  size_t drow, xsplit, dq_acc, drow_s, xsplit_s, dq_acc_s, ctx, total;
+  int chunk, num_chunks, num_parts, self_part;
+  bool tc, atomic;
 };
 
-static BwdLayout bwd_layout(const dkv_bwd_params* p) {
+// Scratch of one backward launch.  `with_self`: the two-call launch, where Call 1 (the prompt's
+// causal self-attention) runs in the same launch and adds into the same fp32 prompt scratch.
+static BwdLayout bwd_layout(const dkv_bwd_params* p, bool with_self) {
   BwdLayout L{};
   const size_t T = static_cast<size_t>(std::max<int64_t>(0, p->total_q));
   const size_t H = static_cast<size_t>(p->heads), Hk = static_cast<size_t>(std::max<int64_t>(1, p->kv_heads));
-  const size_t D = static_cast<size_t>(p->head_dim), P = static_cast<size_t>(p->ctx_len);
+  const size_t D = static_cast<size_t>(p->head_dim), P = static_cast<size_t>(std::max<int64_t>(0, p->ctx_len));
+  with_self = with_self && P > 0;
   L.chunk = auto_chunk(p);
   L.num_chunks = static_cast<int>((p->num_seqs + L.chunk - 1) / L.chunk);
-  const bool tc = tc_bwd_supported(p->dtype, static_cast<int>(p->head_dim), static_cast<int>(p->heads),
-                                   static_cast<int>(p->kv_heads));
+  L.tc = tc_bwd_supported(p->dtype, static_cast<int>(p->head_dim), static_cast<int>(p->heads),
+                          static_cast<int>(p->kv_heads));
+  const int writers = L.num_chunks + (with_self ? 1 : 0);  // independent writers of prompt gradients
   // atomic accumulation into one fp32 plane unless the caller wants ordered / per-chunk partials
-  L.num_parts = (tc && !p->deterministic && !p->ctx_partials) ? 1 : L.num_chunks;
+  L.atomic = L.tc && !p->deterministic && !p->ctx_partials && writers > 1;
+  L.num_parts = L.atomic ? 1 : writers;
+  L.self_part = L.atomic ? 0 : L.num_chunks;
   size_t off = 0;
   L.drow = off;
-  off += align256(H * T * 4);
-  L.dpack = off;  // xsplit: H * tpad rows of 32 bf16
-  off += align256(H * static_cast<size_t>(dpack_tpad(T)) * 64);
+  off += L.tc ? 0 : align256(H * T * 4);
+  L.xsplit = off;  // H * tpad rows of 32 bf16
+  off += L.tc ? align256(H * static_cast<size_t>(dpack_tpad(T)) * 64) : 0;
   L.dq_acc = off;
-  off += tc ? align256(T * H * D * 4) : 0;
+  off += L.tc ? align256(T * H * D * 4) : 0;
+  L.drow_s = off;
+  off += (with_self && !L.tc) ? align256(H * P * 4) : 0;
+  L.xsplit_s = off;
+  off += (with_self && L.tc) ? align256(H * static_cast<size_t>(dpack_tpad(P)) * 64) : 0;
+  L.dq_acc_s = off;
+  off += (with_self && L.tc) ? align256(P * H * D * 4) : 0;
   L.ctx = off;
   off += (p->ctx_partials ? 0 : align256(static_cast<size_t>(L.num_parts) * 2 * P * Hk * D * 4));
   L.total = off;
   return L;
 }
 
-static int bwd_impl(const dkv_bwd_params* p, void* ws, size_t ws_bytes, bool dualkv, void* stream,
-                    const char* fn) {
+static int bwd_impl(const dkv_bwd_params* p, const CtxSelf* self, void* ws, size_t ws_bytes, bool dualkv,
+                    void* stream, const char* fn) {
   int rc = validate_common(p, dualkv, fn);
   if (rc) return rc;
   if (p->total_q > 0 && (!p->out || !p->lse || !p->dout || !p->dq || !p->dk || !p->dv))
     return fail(DKV_ERR_INVALID, std::string(fn) + ": null out/lse/dout/dq/dk/dv");
   if (p->ctx_len > 0 && (!p->dk_ctx || !p->dv_ctx)) return fail(DKV_ERR_INVALID, std::string(fn) + ": null dk_ctx/dv_ctx");
-  BwdLayout L = bwd_layout(p);
+  if (self && p->ctx_len > 0 && (!self->q || !self->out || !self->lse || !self->dout || !self->dq))
+    return fail(DKV_ERR_INVALID, std::string(fn) + ": null q_ctx/out_ctx/lse_ctx/dout_ctx/dq_ctx");
+  const bool with_self = self && p->ctx_len > 0;
+  BwdLayout L = bwd_layout(p, with_self);
   if (ws_bytes < L.total || (L.total > 0 && !ws))
     return fail(DKV_ERR_WORKSPACE, std::string(fn) + ": workspace too small (need " + std::to_string(L.total) + ")");
   auto st = static_cast<cudaStream_t>(stream);
@@ -189,42 +205,89 @@ static int bwd_impl(const dkv_bwd_params* p, void* ws, size_t ws_bytes, bool dua
   a.dq = p->dq;
   a.dk = p->dk;
   a.dv = p->dv;
+  // the fused Call 1 problem: the prompt's own queries, keys = the context tensors
+  SimtArgs s = a;
+  if (with_self) {
+    s.q = self->q;
+    s.k = p->k_ctx;
+    s.v = p->v_ctx;
+    s.out = self->out;
+    s.lse = self->lse;
+    s.dout = self->dout;
+    s.dq = self->dq;
+    s.total_q = static_cast<int>(p->ctx_len);
+    s.num_seqs = 1;
+    s.max_seqlen = static_cast<int>(p->ctx_len);
+    s.ctx_len = 0;
+    s.cu = nullptr;  // one sequence: the prompt
+  }
   const int64_t plane = p->ctx_len * p->kv_heads * p->head_dim;
+  const size_t esz = a.dtype == DKV_F32 ? 4 : 2;
   float* ctx = p->ctx_partials ? p->ctx_partials : reinterpret_cast<float*>(w + L.ctx);
-  const bool tc = tc_bwd_supported(a.dtype, a.head_dim, a.heads, a.kv_heads);
-  if (a.total_q == 0) {
+  if (a.total_q == 0 && !with_self) {
     // no queries: every gradient is zero (test_dualkv.py:96-102)
     if (plane > 0) {
-      cudaMemsetAsync(p->dk_ctx, 0, plane * (a.dtype == DKV_F32 ? 4 : 2), st);
-      cudaMemsetAsync(p->dv_ctx, 0, plane * (a.dtype == DKV_F32 ? 4 : 2), st);
+      cudaMemsetAsync(p->dk_ctx, 0, plane * esz, st);
+      cudaMemsetAsync(p->dv_ctx, 0, plane * esz, st);
       if (p->ctx_partials) cudaMemsetAsync(p->ctx_partials, 0, L.num_chunks * 2 * plane * 4, st);
     }
     return check_launch(fn);
   }
-  float* drow = reinterpret_cast<float*>(w + L.drow);
-  float* dpack = reinterpret_cast<float*>(w + L.dpack);
-  if (tc) {
-    float* dq_acc = reinterpret_cast<float*>(w + L.dq_acc);
-    cudaMemsetAsync(dq_acc, 0, static_cast<size_t>(a.total_q) * a.heads * a.head_dim * 4, st);
-    const bool atomic_ctx = L.num_parts == 1 && L.num_chunks > 1;
-    // chunks whose responses are all empty write nothing: start from zero
-    if (plane > 0) cudaMemsetAsync(ctx, 0, static_cast<size_t>(L.num_parts) * 2 * plane * 4, st);
-    const int tpad = dpack_tpad(static_cast<size_t>(a.total_q));
-    __nv_bfloat16* xsplit = reinterpret_cast<__nv_bfloat16*>(dpack);
-    launch_rowsum_do_o(a, nullptr, xsplit, tpad, st);
+  // parts nobody writes (chunks of empty responses) must read as zero
+  if (plane > 0) cudaMemsetAsync(ctx, 0, static_cast<size_t>(L.num_parts) * 2 * plane * 4, st);
+  if (L.tc) {
+    BwdScratch sc{};
+    sc.dq_acc = reinterpret_cast<float*>(w + L.dq_acc);
+    sc.xsplit = reinterpret_cast<__nv_bfloat16*>(w + L.xsplit);
+    sc.tpad = dpack_tpad(static_cast<size_t>(a.total_q));
+    sc.ctx_acc = ctx;
+    sc.chunk = L.chunk;
+    sc.num_chunks = L.num_chunks;
+    sc.self_part = L.self_part;
+    sc.atomic_ctx = L.atomic;
+    if (a.total_q > 0) {
+      cudaMemsetAsync(sc.dq_acc, 0, static_cast<size_t>(a.total_q) * a.heads * a.head_dim * 4, st);
+      launch_rowsum_do_o(a, nullptr, const_cast<__nv_bfloat16*>(sc.xsplit), sc.tpad, st);
+      prof_count(1);
+    }
+    if (with_self) {
+      sc.dq_acc_s = reinterpret_cast<float*>(w + L.dq_acc_s);
+      sc.xsplit_s = reinterpret_cast<__nv_bfloat16*>(w + L.xsplit_s);
+      sc.tpad_s = dpack_tpad(static_cast<size_t>(p->ctx_len));
+      cudaMemsetAsync(sc.dq_acc_s, 0, static_cast<size_t>(p->ctx_len) * a.heads * a.head_dim * 4, st);
+      launch_rowsum_do_o(s, nullptr, const_cast<__nv_bfloat16*>(sc.xsplit_s), sc.tpad_s, st);
+      prof_count(1);
+    }
     prof_main_begin(1, st);
-    rc = launch_tc_bwd(a, dq_acc, xsplit, tpad, ctx, L.chunk, L.num_chunks, atomic_ctx, st);
+    rc = launch_tc_bwd(a, with_self ? self : nullptr, sc, st);
     if (rc) return rc;
     prof_main_end(1, st);
     // the kernel accumulates dQ / softmax_scale (the scale is folded into this single cast)
-    launch_convert(dq_acc, p->dq, a.dtype, static_cast<int64_t>(a.total_q) * a.heads * a.head_dim, st, a.scale);
-    prof_count(3);
+    if (a.total_q > 0) {
+      launch_convert(sc.dq_acc, p->dq, a.dtype, static_cast<int64_t>(a.total_q) * a.heads * a.head_dim, st, a.scale);
+      prof_count(1);
+    }
+    if (with_self) {
+      launch_convert(sc.dq_acc_s, self->dq, a.dtype, plane / p->kv_heads * p->heads, st, a.scale);
+      prof_count(1);
+    }
+    prof_count(1);
   } else {
-    launch_rowsum_do_o(a, drow, nullptr, 0, st);
+    float* drow = reinterpret_cast<float*>(w + L.drow);
     prof_main_begin(1, st);
-    launch_simt_bwd(a, drow, L.chunk, L.num_chunks, ctx, st);
+    if (a.total_q > 0) {
+      launch_rowsum_do_o(a, drow, nullptr, 0, st);
+      launch_simt_bwd(a, drow, L.chunk, L.num_chunks, ctx, nullptr, st);
+      prof_count(3);
+    }
+    if (with_self) {
+      // Call 1's prompt-key gradient lands in fp32 as the last part: still one cast in total
+      float* drow_s = reinterpret_cast<float*>(w + L.drow_s);
+      launch_rowsum_do_o(s, drow_s, nullptr, 0, st);
+      launch_simt_bwd(s, drow_s, 1, 1, nullptr, ctx + static_cast<int64_t>(L.self_part) * 2 * plane, st);
+      prof_count(3);
+    }
     prof_main_end(1, st);
-    prof_count(3);
   }
   if (plane > 0) {
     launch_fold_convert(ctx, L.num_parts, plane, p->dk_ctx, p->dv_ctx, a.dtype, st);
@@ -288,17 +351,68 @@ int32_t dkv_varlen_fwd(const dkv_fwd_params* p, void* stream) { return fwd_impl(
 
 size_t dkv_bwd_workspace_size(const dkv_bwd_params* p) {
   if (!p) return 0;
-  return bwd_layout(p).total;
+  return bwd_layout(p, false).total;
 }
 int64_t dkv_bwd_num_ctx_chunks(const dkv_bwd_params* p) {
   if (!p) return 0;
-  return bwd_layout(p).num_chunks;
+  return bwd_layout(p, false).num_chunks;
 }
 int32_t dkv_dualkv_bwd(const dkv_bwd_params* p, void* ws, size_t ws_bytes, void* stream) {
-  return bwd_impl(p, ws, ws_bytes, true, stream, "dkv_dualkv_bwd");
+  return bwd_impl(p, nullptr, ws, ws_bytes, true, stream, "dkv_dualkv_bwd");
 }
 int32_t dkv_varlen_bwd(const dkv_bwd_params* p, void* ws, size_t ws_bytes, void* stream) {
-  return bwd_impl(p, ws, ws_bytes, false, stream, "dkv_varlen_bwd");
+  return bwd_impl(p, nullptr, ws, ws_bytes, false, stream, "dkv_varlen_bwd");
+}
+
+int32_t dkv_twocall_fwd(const dkv_twocall_fwd_params* p, void* stream) {
+  if (!p) return fail(DKV_ERR_INVALID, "dkv_twocall_fwd: null params");
+  const dkv_fwd_params* c = &p->call2;
+  int rc = validate_common(c, true, "dkv_twocall_fwd");
+  if (rc) return rc;
+  if (c->total_q > 0 && (!c->out || !c->lse)) return fail(DKV_ERR_INVALID, "dkv_twocall_fwd: null out/lse");
+  if (c->ctx_len > 0 && (!p->q_ctx || !p->out_ctx || !p->lse_ctx))
+    return fail(DKV_ERR_INVALID, "dkv_twocall_fwd: null q_ctx/out_ctx/lse_ctx");
+  SimtArgs a = to_args(c);
+  a.out = c->out;
+  a.lse = c->lse;
+  auto st = static_cast<cudaStream_t>(stream);
+  CtxSelf self{p->q_ctx, p->out_ctx, p->lse_ctx, nullptr, nullptr};
+  prof_main_begin(0, st);
+  if (tc_supported(a.dtype, a.head_dim, a.heads, a.kv_heads)) {
+    rc = launch_tc_fwd(a, c->ctx_len > 0 ? &self : nullptr, st);
+    if (rc) return rc;
+  } else {
+    if (a.total_q > 0) launch_simt_fwd(a, st);
+    if (c->ctx_len > 0) {
+      SimtArgs s = a;
+      s.q = p->q_ctx;
+      s.k = c->k_ctx;
+      s.v = c->v_ctx;
+      s.out = p->out_ctx;
+      s.lse = p->lse_ctx;
+      s.total_q = static_cast<int>(c->ctx_len);
+      s.num_seqs = 1;
+      s.max_seqlen = s.total_q;
+      s.ctx_len = 0;
+      s.cu = nullptr;  // one sequence: the prompt
+      launch_simt_fwd(s, st);
+    }
+  }
+  prof_main_end(0, st);
+  prof_count(1);
+  return check_launch("dkv_twocall_fwd");
+}
+
+size_t dkv_twocall_bwd_workspace_size(const dkv_twocall_bwd_params* p) {
+  if (!p) return 0;
+  return bwd_layout(&p->call2, true).total;
+}
+
+int32_t dkv_twocall_bwd(const dkv_twocall_bwd_params* p, void* ws, size_t ws_bytes, void* stream) {
+  if (!p) return fail(DKV_ERR_INVALID, "dkv_twocall_bwd: null params");
+  if (p->call2.ctx_partials) return fail(DKV_ERR_INVALID, "dkv_twocall_bwd: ctx_partials is not supported");
+  CtxSelf self{p->q_ctx, const_cast<void*>(p->out_ctx), const_cast<float*>(p->lse_ctx), p->dout_ctx, p->dq_ctx};
+  return bwd_impl(&p->call2, &self, ws, ws_bytes, true, stream, "dkv_twocall_bwd");
 }
 
 }  // extern "C"

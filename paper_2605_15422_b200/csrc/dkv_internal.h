@@ -15,7 +15,7 @@ struct SimtArgs {
   const void* v_ctx;
   const void* k;
   const void* v;
-  const int32_t* cu;
+  const int32_t* cu;  // null: one sequence of total_q rows
   void* out;
   float* lse;
   const void* dout;
@@ -35,6 +35,16 @@ struct SimtArgs {
 
 void set_error(const std::string& msg);
 
+// Call 1 of the two-call decomposition fused into a Call 2 launch: the prompt's own queries
+// (rows [0, ctx_len) of q/out/dout/dq below) attend causally to the context keys.
+struct CtxSelf {
+  const void* q;     // [P, H, d]
+  void* out;         // [P, H, d]
+  float* lse;        // [H, P]
+  const void* dout;  // backward only
+  void* dq;          // backward only
+};
+
 // profiling hooks (dkv_abi.cu): kind 0 = forward main kernel, 1 = backward main kernel
 void prof_main_begin(int kind, cudaStream_t st);
 void prof_main_end(int kind, cudaStream_t st);
@@ -42,8 +52,9 @@ void prof_count(int launches);
 
 // simt_attn.cu
 void launch_simt_fwd(const SimtArgs& a, cudaStream_t st);
+// own_part (may be null): write own-row dK/dV as fp32 [2][rows][Hk][D] instead of storage dtype
 void launch_simt_bwd(const SimtArgs& a, const float* drow, int chunk, int num_chunks, float* ctx_part,
-                     cudaStream_t st);
+                     float* own_part, cudaStream_t st);
 
 // aux.cu
 // D = rowsum(dO*O) into drow [H][T] (SIMT path) and/or the tensor-core path's split-bf16
@@ -57,11 +68,22 @@ void launch_convert(const float* src, void* dst, int dtype, int64_t n, cudaStrea
 bool force_simt();  // DKV_FORCE_SIMT=1: route everything to the SIMT kernels (cross-checks)
 bool tc_supported(int dtype, int head_dim, int heads, int kv_heads);
 bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads);
-int launch_tc_fwd(const SimtArgs& a, cudaStream_t st);
-// dq_acc [T,H,D] f32 (pre-zeroed; holds dQ / softmax_scale), xsplit from launch_rowsum_do_o,
-// ctx_acc f32
-// [num_parts][2][P][Hk][D] (pre-zeroed when atomic), `atomic_ctx`: parts are red.add'ed.
-int launch_tc_bwd(const SimtArgs& a, float* dq_acc, const __nv_bfloat16* xsplit, int tpad, float* ctx_acc, int chunk,
-                  int num_chunks, bool atomic_ctx, cudaStream_t st);
+int launch_tc_fwd(const SimtArgs& a, const CtxSelf* self, cudaStream_t st);
+// Backward scratch: dq_acc [T,H,D] f32 (pre-zeroed; accumulates dQ / softmax_scale), xsplit from
+// launch_rowsum_do_o; the *_s fields are the fused Call 1's (prompt rows); ctx_acc f32
+// [parts][2][P][Hk][D] pre-zeroed: chunk c writes part c (or every item red.adds part 0 when
+// atomic_ctx), fused Call 1 items write part self_part.
+struct BwdScratch {
+  float* dq_acc;
+  const __nv_bfloat16* xsplit;
+  int tpad;
+  float* dq_acc_s;
+  const __nv_bfloat16* xsplit_s;
+  int tpad_s;
+  float* ctx_acc;
+  int chunk, num_chunks, self_part;
+  bool atomic_ctx;
+};
+int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, cudaStream_t st);
 
 }  // namespace dkv

@@ -47,11 +47,15 @@ struct Cfg {
 
 struct Params {
   CUtensorMap tm_q, tm_k, tm_v, tm_kc, tm_vc;
+  CUtensorMap tm_qs;      // fused Call 1: the prompt's own queries [P, H, d]
   __nv_bfloat16* out;
   float* lse;
+  __nv_bfloat16* out_s;   // fused Call 1 outputs [P, H, d], lse [H, P]
+  float* lse_s;
   const int32_t* cu;
-  int num_seqs, total_q, ctx_len, heads, kv_heads, group, tq, blocks_per_seq_max;
-  float scale_log2;  // softmax_scale * log2(e)
+  int num_seqs, total_q, ctx_len, heads, kv_heads, group, tq;
+  int n_main_items;       // items >= n_main_items are Call 1 items (causal self-attention over the prompt)
+  float scale_log2;       // softmax_scale * log2(e)
 };
 
 struct Smem {
@@ -71,13 +75,43 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
   uint8_t* sV = sK + C::kStages * C::kTileBytes;
   Smem& sm = *reinterpret_cast<Smem*>(base + C::kSmemTiles);
 
-  // ---- work item: (q-block pair counted from the sequence end, sequence, kv head)
-  const int hk = blockIdx.x % p.kv_heads;
-  const int rest = blockIdx.x / p.kv_heads;
-  const int seq = rest % p.num_seqs;
-  const int jb = rest / p.num_seqs;
-  const int seq0 = p.cu[seq];
-  const int rlen = p.cu[seq + 1] - seq0;
+  // ---- work item.  Main items: (q-block pair counted from the sequence end, sequence, kv head)
+  // of the two-region problem.  Fused Call 1 items (two-call launch only): the prompt's own
+  // queries attend causally to the prompt keys -- one more "sequence" whose own-region K/V are
+  // the context tensors and which has no context region.
+  const bool self_item = static_cast<int>(blockIdx.x) >= p.n_main_items;
+  int hk, jb, seq0, rlen, n_ctx, lse_stride;
+  const CUtensorMap *mq, *mk_own, *mv_own;
+  __nv_bfloat16* out;
+  float* lse_out;
+  if (!self_item) {
+    hk = blockIdx.x % p.kv_heads;
+    const int rest = blockIdx.x / p.kv_heads;
+    const int seq = rest % p.num_seqs;
+    jb = rest / p.num_seqs;
+    seq0 = p.cu[seq];
+    rlen = p.cu[seq + 1] - seq0;
+    n_ctx = (p.ctx_len + kBN - 1) / kBN;
+    mq = &p.tm_q;
+    mk_own = &p.tm_k;
+    mv_own = &p.tm_v;
+    out = p.out;
+    lse_out = p.lse;
+    lse_stride = p.total_q;
+  } else {
+    const int b = blockIdx.x - p.n_main_items;
+    hk = b % p.kv_heads;
+    jb = b / p.kv_heads;
+    seq0 = 0;
+    rlen = p.ctx_len;
+    n_ctx = 0;
+    mq = &p.tm_qs;
+    mk_own = &p.tm_kc;
+    mv_own = &p.tm_vc;
+    out = p.out_s;
+    lse_out = p.lse_s;
+    lse_stride = p.ctx_len;
+  }
   const int pair_tok = 2 * p.tq;
   const int nblk = (rlen + pair_tok - 1) / pair_tok;
   if (jb >= nblk) return;
@@ -85,7 +119,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
   const bool has_b = tok0 + p.tq < rlen;
   const int last_tok = min(tok0 + pair_tok, rlen) - 1;
   const int n_own = last_tok / kBN + 1;
-  const int n_ctx = (p.ctx_len + kBN - 1) / kBN;
   const int n_iter = n_own + n_ctx;
 
   const int warp = warp_id();
@@ -125,9 +158,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
   if (warp == 8) {
     // ================= TMA producer
     if (elect_one()) {
-      tma_prefetch(&p.tm_q);
-      tma_prefetch(&p.tm_k);
-      tma_prefetch(&p.tm_v);
+      tma_prefetch(mq);
+      tma_prefetch(mk_own);
+      tma_prefetch(mv_own);
       if (n_ctx > 0) {
         tma_prefetch(&p.tm_kc);
         tma_prefetch(&p.tm_vc);
@@ -137,15 +170,15 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
       mbar_arrive_expect_tx(&sm.q_full, qbytes);
       for (int t = 0; t < (has_b ? 2 : 1); ++t)
         for (int pn = 0; pn < C::kPanels; ++pn)
-          tma_load_3d(sQ[t] + pn * C::kPanelBytes, &p.tm_q, &sm.q_full, pn * 64, hk * p.group,
+          tma_load_3d(sQ[t] + pn * C::kPanelBytes, mq, &sm.q_full, pn * 64, hk * p.group,
                       seq0 + tok0 + t * p.tq);
       for (int it = 0; it < n_iter; ++it) {
         bool is_ctx;
         const int j = tile_of(it, is_ctx);
         const int slot = it % C::kStages;
         const uint32_t ph = (it / C::kStages) & 1;
-        const CUtensorMap* mk = is_ctx ? &p.tm_kc : &p.tm_k;
-        const CUtensorMap* mv = is_ctx ? &p.tm_vc : &p.tm_v;
+        const CUtensorMap* mk = is_ctx ? &p.tm_kc : mk_own;
+        const CUtensorMap* mv = is_ctx ? &p.tm_vc : mv_own;
         const int row = is_ctx ? j * kBN : seq0 + j * kBN;
         mbar_wait(&sm.k_empty[slot], ph ^ 1);
         mbar_arrive_expect_tx(&sm.k_full[slot], C::kTileBytes);
@@ -310,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
       mbar_wait(&sm.o_full[t], 0);
       tc_fence_after();
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      __nv_bfloat16* orow = p.out + (static_cast<int64_t>(seq0 + qtok) * p.heads + head) * D;
+      __nv_bfloat16* orow = out + (static_cast<int64_t>(seq0 + qtok) * p.heads + head) * D;
 #pragma unroll 1
       for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t r[32];
@@ -328,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         }
       }
       if (row_valid)
-        p.lse[static_cast<int64_t>(head) * p.total_q + seq0 + qtok] =
+        lse_out[static_cast<int64_t>(head) * lse_stride + seq0 + qtok] =
             (m_run + __log2f(l_run)) * 0.6931471805599453f;
     }
   }
@@ -341,14 +374,15 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
 }
 
 template <int D>
-int launch(const SimtArgs& a, cudaStream_t st) {
+int launch(const SimtArgs& a, const CtxSelf* self, cudaStream_t st) {
   using C = Cfg<D>;
   Params p{};
   const int G = a.heads / a.kv_heads;
   const int tq = kBM / G;
-  if (!make_map_3d_bf16(&p.tm_q, a.q, a.total_q, a.heads, D, G, tq) ||
-      !make_map_3d_bf16(&p.tm_k, a.k, a.total_q, a.kv_heads, D, 1, kBN) ||
-      !make_map_3d_bf16(&p.tm_v, a.v, a.total_q, a.kv_heads, D, 1, kBN)) {
+  if (a.total_q > 0 &&
+      (!make_map_3d_bf16(&p.tm_q, a.q, a.total_q, a.heads, D, G, tq) ||
+       !make_map_3d_bf16(&p.tm_k, a.k, a.total_q, a.kv_heads, D, 1, kBN) ||
+       !make_map_3d_bf16(&p.tm_v, a.v, a.total_q, a.kv_heads, D, 1, kBN))) {
     set_error("cuTensorMapEncodeTiled failed for q/k/v");
     return DKV_ERR_CUDA;
   }
@@ -359,8 +393,15 @@ int launch(const SimtArgs& a, cudaStream_t st) {
       return DKV_ERR_CUDA;
     }
   }
+  const bool with_self = self && a.ctx_len > 0;
+  if (with_self && !make_map_3d_bf16(&p.tm_qs, self->q, a.ctx_len, a.heads, D, G, tq)) {
+    set_error("cuTensorMapEncodeTiled failed for q_ctx");
+    return DKV_ERR_CUDA;
+  }
   p.out = static_cast<__nv_bfloat16*>(a.out);
   p.lse = a.lse;
+  p.out_s = with_self ? static_cast<__nv_bfloat16*>(self->out) : nullptr;
+  p.lse_s = with_self ? self->lse : nullptr;
   p.cu = a.cu;
   p.num_seqs = a.num_seqs;
   p.total_q = a.total_q;
@@ -370,13 +411,17 @@ int launch(const SimtArgs& a, cudaStream_t st) {
   p.group = G;
   p.tq = tq;
   p.scale_log2 = a.scale * 1.4426950408889634f;
-  const int blocks_per_seq = (a.max_seqlen + 2 * tq - 1) / (2 * tq);
-  const int64_t grid = static_cast<int64_t>(blocks_per_seq) * a.num_seqs * a.kv_heads;
+  const int blocks_per_seq = a.total_q > 0 ? (a.max_seqlen + 2 * tq - 1) / (2 * tq) : 0;
+  const int64_t main_items = static_cast<int64_t>(blocks_per_seq) * a.num_seqs * a.kv_heads;
+  const int64_t self_items =
+      with_self ? static_cast<int64_t>((a.ctx_len + 2 * tq - 1) / (2 * tq)) * a.kv_heads : 0;
+  const int64_t grid = main_items + self_items;  // Call 1 items run in the tail of Call 2's
   if (grid == 0) return DKV_OK;
   if (grid > 0x7fffffff) {
     set_error("forward grid too large");
     return DKV_ERR_UNSUPPORTED;
   }
+  p.n_main_items = static_cast<int>(main_items);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(dualkv_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
@@ -404,9 +449,9 @@ bool tc_supported(int dtype, int head_dim, int heads, int kv_heads) {
   return G <= 128 && (128 % G) == 0;
 }
 
-int launch_tc_fwd(const SimtArgs& a, cudaStream_t st) {
-  if (a.head_dim == 128) return fwd::launch<128>(a, st);
-  return fwd::launch<64>(a, st);
+int launch_tc_fwd(const SimtArgs& a, const CtxSelf* self, cudaStream_t st) {
+  if (a.head_dim == 128) return fwd::launch<128>(a, self, st);
+  return fwd::launch<64>(a, self, st);
 }
 
 }  // namespace dkv

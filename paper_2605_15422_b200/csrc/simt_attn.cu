@@ -32,8 +32,13 @@ DKV_DEVICE float warp_sum(float v) {
 
 constexpr int kMaxPerLane = 8;  // head_dim <= 256
 
+// cu_seqlens entry i; a null cu means one sequence spanning all total_q rows (the prompt of a
+// fused two-call launch)
+DKV_DEVICE int cu_at(const SimtArgs& a, int i) { return a.cu ? a.cu[i] : (i == 0 ? 0 : a.total_q); }
+
 // binary search: sequence containing packed row t
 DKV_DEVICE int seq_of_row(const int32_t* cu, int n, int t) {
+  if (!cu) return 0;
   int lo = 0, hi = n - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
@@ -52,8 +57,8 @@ __global__ void simt_fwd_kernel(SimtArgs a) {
   const int t = gw / a.heads, h = gw % a.heads;
   const int hk = h / (a.heads / a.kv_heads);
   const int s = seq_of_row(a.cu, a.num_seqs, t);
-  const int r = t - a.cu[s];
-  const int seq0 = a.cu[s];
+  const int r = t - cu_at(a, s);
+  const int seq0 = cu_at(a, s);
   const int D = a.head_dim;
   const T* q = static_cast<const T*>(a.q) + (static_cast<int64_t>(t) * a.heads + h) * D;
   float qr[kMaxPerLane], acc[kMaxPerLane];
@@ -109,8 +114,8 @@ __global__ void simt_bwd_dq_kernel(SimtArgs a, const float* drow) {
   const int t = gw / a.heads, h = gw % a.heads;
   const int hk = h / (a.heads / a.kv_heads);
   const int s = seq_of_row(a.cu, a.num_seqs, t);
-  const int r = t - a.cu[s];
-  const int seq0 = a.cu[s];
+  const int r = t - cu_at(a, s);
+  const int seq0 = cu_at(a, s);
   const int D = a.head_dim;
   const int64_t qoff = (static_cast<int64_t>(t) * a.heads + h) * D;
   float qr[kMaxPerLane], gr[kMaxPerLane], dq[kMaxPerLane];
@@ -163,7 +168,7 @@ __global__ void simt_bwd_dq_kernel(SimtArgs a, const float* drow) {
 // fp32 partial (instrumentation / deterministic fold).
 template <typename T>
 __global__ void simt_bwd_dkv_kernel(SimtArgs a, const float* drow, int own_rows, int chunk,
-                                    int num_chunks, float* ctx_part) {
+                                    int num_chunks, float* ctx_part, float* own_part) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int D = a.head_dim;
@@ -178,7 +183,7 @@ __global__ void simt_bwd_dkv_kernel(SimtArgs a, const float* drow, int own_rows,
     const int t = gw / a.kv_heads;
     hk = gw % a.kv_heads;
     const int s = seq_of_row(a.cu, a.num_seqs, t);
-    j = t - a.cu[s];
+    j = t - cu_at(a, s);
     s_lo = s;
     s_hi = s + 1;
     kb = static_cast<const T*>(a.k);
@@ -194,7 +199,7 @@ __global__ void simt_bwd_dkv_kernel(SimtArgs a, const float* drow, int own_rows,
     kb = static_cast<const T*>(a.k_ctx);
     vb = static_cast<const T*>(a.v_ctx);
   }
-  const int64_t krow = is_ctx ? j : (a.cu[s_lo] + j);
+  const int64_t krow = is_ctx ? j : (cu_at(a, s_lo) + j);
   const int64_t ko = (krow * a.kv_heads + hk) * D;
   float kr[kMaxPerLane], vr[kMaxPerLane], dk[kMaxPerLane], dv[kMaxPerLane];
 #pragma unroll
@@ -206,7 +211,7 @@ __global__ void simt_bwd_dkv_kernel(SimtArgs a, const float* drow, int own_rows,
     dv[i] = 0.f;
   }
   for (int s = s_lo; s < s_hi; ++s) {
-    const int r0 = a.cu[s], r1 = a.cu[s + 1];
+    const int r0 = cu_at(a, s), r1 = cu_at(a, s + 1);
     const int first = is_ctx ? r0 : r0 + j;
     for (int t = first; t < r1; ++t) {
       for (int g = 0; g < G; ++g) {
@@ -234,7 +239,18 @@ __global__ void simt_bwd_dkv_kernel(SimtArgs a, const float* drow, int own_rows,
       }
     }
   }
-  if (!is_ctx) {
+  if (!is_ctx && own_part) {
+    // fp32 [2][rows][Hk][D] (fused Call 1 of a two-call backward: cast once later, with Call 2's)
+    const int64_t plane = static_cast<int64_t>(own_rows) * a.kv_heads * D;
+#pragma unroll
+    for (int i = 0; i < kMaxPerLane; ++i) {
+      int e = lane + 32 * i;
+      if (e < D) {
+        own_part[ko + e] = dk[i];
+        own_part[plane + ko + e] = dv[i];
+      }
+    }
+  } else if (!is_ctx) {
 #pragma unroll
     for (int i = 0; i < kMaxPerLane; ++i) {
       int e = lane + 32 * i;
@@ -271,7 +287,7 @@ void launch_simt_fwd(const SimtArgs& a, cudaStream_t st) {
 }
 
 void launch_simt_bwd(const SimtArgs& a, const float* drow, int chunk, int num_chunks, float* ctx_part,
-                     cudaStream_t st) {
+                     float* own_part, cudaStream_t st) {
   const int threads = 256;
   const int64_t w1 = a.total_q * a.heads;
   if (w1 > 0) {
@@ -286,10 +302,10 @@ void launch_simt_bwd(const SimtArgs& a, const float* drow, int chunk, int num_ch
     const int64_t b2 = (w2 * 32 + threads - 1) / threads;
     if (a.dtype == DKV_F32)
       simt_bwd_dkv_kernel<float><<<b2, threads, 0, st>>>(a, drow, static_cast<int>(a.total_q), chunk,
-                                                         num_chunks, ctx_part);
+                                                         num_chunks, ctx_part, own_part);
     else
       simt_bwd_dkv_kernel<__nv_bfloat16><<<b2, threads, 0, st>>>(a, drow, static_cast<int>(a.total_q),
-                                                                 chunk, num_chunks, ctx_part);
+                                                                 chunk, num_chunks, ctx_part, own_part);
   }
 }
 
