@@ -134,11 +134,13 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
   int kind, hk, ktile, s0, s1, tok_first, kv_len, kv_row0, part = 0;
   if (bid < p.n_ctx_items) {
     kind = 0;
+    // key tiles fastest: the ~148 co-resident CTAs then share a few (chunk, head) Q/dO streams
+    // and dQ-accumulator regions in L2 instead of 8 heads' worth
     const int per_chunk = p.n_ctx_tiles * p.kv_heads;
     const int chunk_id = bid / per_chunk;
     const int rem = bid % per_chunk;
-    ktile = rem / p.kv_heads;
-    hk = rem % p.kv_heads;
+    ktile = rem % p.n_ctx_tiles;
+    hk = rem / p.n_ctx_tiles;
     s0 = chunk_id * p.chunk;
     s1 = min(p.num_seqs, s0 + p.chunk);
     tok_first = 0;
@@ -160,8 +162,8 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
   } else {
     kind = 2;
     const int b3 = bid - p.n_ctx_items;
-    hk = b3 % p.kv_heads;
-    ktile = b3 / p.kv_heads;
+    ktile = b3 % p.n_ctx_tiles;
+    hk = b3 / p.n_ctx_tiles;
     s0 = 0;
     s1 = 1;
     kv_len = p.ctx_len;
@@ -242,7 +244,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         tma_load_3d(base + kOffV + pn * kKVPanel, mv, &bar.kv_full, pn * 64, hk, kv_row0 + kbase);
       }
     }
-    const uint64_t pol_q = policy_evict_last();
     if (lane == 0) {
       QIter it;
       it.begin(cu, p.tq, s0, s1, tok_first);
@@ -253,10 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         const int row0 = cu[it.s] + it.tok;
         mbar_arrive_expect_tx(&bar.q_full[st], 2 * kQBytes + 2 * kXBytes);
         for (int pn = 0; pn < 2; ++pn) {
-          tma_load_3d_hint(base + kOffQ + st * kQBytes + pn * kQPanel, mq, &bar.q_full[st], pn * 64,
-                           hk * G, row0, pol_q);
-          tma_load_3d_hint(base + kOffDO + st * kQBytes + pn * kQPanel, mdo, &bar.q_full[st], pn * 64,
-                           hk * G, row0, pol_q);
+          tma_load_3d(base + kOffQ + st * kQBytes + pn * kQPanel, mq, &bar.q_full[st], pn * 64, hk * G, row0);
+          tma_load_3d(base + kOffDO + st * kQBytes + pn * kQPanel, mdo, &bar.q_full[st], pn * 64, hk * G, row0);
         }
         // the tile's 64 additive-constant rows: -lse/scale (cols 0-15) and -D (cols 16-31)
         const int xrow = (hk * xtpad + row0) * G;
