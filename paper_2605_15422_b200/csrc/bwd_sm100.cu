@@ -33,6 +33,8 @@
 #include "dkv_internal.h"
 #include "tma_host.h"
 
+#include <cstdlib>
+
 namespace dkv {
 namespace bwd {
 
@@ -75,6 +77,7 @@ struct Params {
   int num_seqs, total_q, ctx_len, heads, kv_heads, group, tq, tpad;
   int chunk, n_ctx_items, n_ctx_tiles;
   int atomic_ctx;
+  int ablate;  // timing experiments only (DKV_BWD_ABLATE): 1 drain I/O, 2 compute math, 4 Q/dO loads
   float scale, scale_log2;
 };
 
@@ -252,8 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         const uint32_t ph = (i / kStages) & 1;
         mbar_wait(&bar.q_empty[st], ph ^ 1);
         const int row0 = cu[it.s] + it.tok;
-        mbar_arrive_expect_tx(&bar.q_full[st], 2 * kQBytes + 2 * kXBytes);
-        for (int pn = 0; pn < 2; ++pn) {
+        mbar_arrive_expect_tx(&bar.q_full[st], ((p.ablate & 4) ? 0 : 2 * kQBytes) + 2 * kXBytes);
+        for (int pn = 0; pn < 2 && !(p.ablate & 4); ++pn) {
           tma_load_3d(base + kOffQ + st * kQBytes + pn * kQPanel, mq, &bar.q_full[st], pn * 64, hk * G, row0);
           tma_load_3d(base + kOffDO + st * kQBytes + pn * kQPanel, mdo, &bar.q_full[st], pn * 64, hk * G, row0);
         }
@@ -364,7 +367,13 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       uint32_t pp[32], pd[32];
       // S' = S - lse/scale and dP' = dP - D arrive from the MMA: P = exp2(S' scale log2e),
       // dS = P dP' (the softmax scale is applied once to dK in the epilogue and dQ in its cast)
-      if (__all_sync(0xffffffffu, cmin == 0 && cmax == kBQ)) {
+      if (p.ablate & 2) {
+#pragma unroll
+        for (int c2 = 0; c2 < 32; ++c2) {
+          pp[c2] = us[2 * c2] ^ us[2 * c2 + 1];
+          pd[c2] = ud[2 * c2] ^ ud[2 * c2 + 1];
+        }
+      } else if (__all_sync(0xffffffffu, cmin == 0 && cmax == kBQ)) {
 #pragma unroll
         for (int c2 = 0; c2 < 32; ++c2) {
           const float e0 = ex2(__uint_as_float(us[2 * c2]) * sl2);
@@ -418,6 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       mbar_arrive(&bar.dq_empty);
       // transpose through smem ([row][d] fp32) and reduce-add the tile into dq_acc with one
       // TMA bulk tensor reduce
+      if (p.ablate & 1) continue;
       float* stg = reinterpret_cast<float*>(base + kOffStage);
       if (threadIdx.x == 128) bulk_wait_read<0>();  // the previous tile's reduce has read the staging
       named_bar_sync(1, 128);
@@ -548,6 +558,10 @@ int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, c
   p.n_self_items = with_self ? p.n_ctx_tiles * a.kv_heads : 0;
   p.self_part = w.self_part;
   p.atomic_ctx = w.atomic_ctx ? 1 : 0;
+  {
+    const char* e = getenv("DKV_BWD_ABLATE");
+    p.ablate = e ? atoi(e) : 0;
+  }
   p.scale = a.scale;
   p.scale_log2 = a.scale * 1.4426950408889634f;
   const int max_tiles = a.total_q > 0 ? (a.max_seqlen + kBK - 1) / kBK : 0;
