@@ -40,6 +40,25 @@ sys.path.insert(0, ROOT)
 
 METRIC = "DualKV attn fwd+bwd ms & TFLOP/s at Qwen3-8B shapes N=32,P=8K; speedup vs N-copy"
 C3 = dict(n=32, p=8192, r=2048, h=32, hk=8, d=128)
+# BASELINE.json configs.  groups: prompt groups per GPU (weak) or in total (strong)
+CONFIGS = {
+    "C1": dict(n=4, p=256, r=128, h=8, hk=8, d=64, dtype="f32", groups=1, scaling="weak",
+               desc="C1: N=4 P=256 R=128 H=Hk=8 d=64 fp32 (latency-bound parity config)"),
+    "C2": dict(n=16, p=4096, r=1024, h=32, hk=8, d=128, dtype="bf16", groups=1, scaling="weak",
+               desc="C2: Qwen3-8B attention N=16 P=4K R=1K"),
+    "C3": dict(n=32, p=8192, r=2048, h=32, hk=8, d=128, dtype="bf16", groups=1, scaling="weak",
+               desc="C3: Qwen3-8B attention, one prompt group N=32 P=8K R=2K per GPU"),
+    "C4": dict(n=16, p=8192, r="ragged", h=32, hk=8, d=128, dtype="bf16", groups=64, scaling="strong",
+               desc="C4: 64 DAPO groups N=16 P=8K R_i~U[512,4096] (rng seed = group), LPT over GPUs"),
+    "C5": dict(n=32, p=16384, r=2048, h=32, hk=4, d=128, dtype="bf16", groups=8, scaling="weak",
+               desc="C5: Qwen3-30B-A3B attention (32/4 heads) N=32 P=16K R=2K, 8 groups per GPU"),
+}
+
+
+def group_r_list(cfg, gidx):
+    if cfg["r"] == "ragged":
+        return [int(x) for x in np.random.default_rng(gidx).integers(512, 4097, cfg["n"])]
+    return [cfg["r"]] * cfg["n"]
 CPU_SAMPLE = dict(n=4, p=2048, r=512, h=32, hk=8, d=128)  # same head config, fewer tokens
 
 
@@ -184,6 +203,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-replicated", action="store_true")
@@ -191,12 +211,15 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
+    import ctypes
+
     import torch
     import torch.distributed as dist
 
     import paper_2605_15422_b200 as dkv
     from paper_2605_15422_b200._lib import lib
-    import ctypes
+    from paper_2605_15422_b200.costmodel import visible_pairs
+    from paper_2605_15422_b200.dp import group_cost, lpt_assign
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -205,31 +228,43 @@ def main():
     if world > 1:
         dist.init_process_group("nccl")
     dev = torch.device("cuda", local)
-    c = C3
-    n, p, r, h, hk, d = c["n"], c["p"], c["r"], c["h"], c["hk"], c["d"]
-    t = n * r
+    cfg = CONFIGS[args.config]
+    p, h, hk, d = cfg["p"], cfg["h"], cfg["hk"], cfg["d"]
+    dt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
+
+    # ---- the prompt groups this rank owns (whole groups only)
+    if cfg["scaling"] == "strong":
+        all_r = [group_r_list(cfg, gi) for gi in range(cfg["groups"])]
+        owned = lpt_assign([group_cost(p, rl) for rl in all_r], world)[rank]
+        my_r = [all_r[gi] for gi in owned]
+        job_r = all_r
+    else:
+        my_r = [group_r_list(cfg, rank * cfg["groups"] + i) for i in range(cfg["groups"])]
+        job_r = None  # every rank the same work
+    pairs_rank = sum(visible_pairs(p, rl, "dualkv") for rl in my_r)
+    fl_rank = 14 * pairs_rank * h * d
+    if job_r is not None:
+        fl_job = 14 * sum(visible_pairs(p, rl, "dualkv") for rl in job_r) * h * d
+    else:
+        fl_job = fl_rank * world
+
+    # buffers sized for the largest group; each group views a prefix (work depends on shape only)
+    tmax = max(sum(rl) for rl in my_r) if my_r else 0
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    mk = lambda *s: torch.randn(*s, device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
-    # one prompt group per rank: prompt q/k/v (Call 1) shared with Call 2's context KV
-    qc, kc, vc = mk(p, h, d), mk(p, hk, d), mk(p, hk, d)
-    q, kd, vd = mk(t, h, d), mk(t, hk, d), mk(t, hk, d)
-    doc, dod = mk(p, h, d), mk(t, h, d)
-    cu = np.arange(0, t + 1, r, dtype=np.int64)
-    cuc = np.array([0, p], dtype=np.int64)
-    ctx_b = dkv.VarlenBatch(qc, kc, vc, cuc)
-    dec = dkv.DualKVInput(q, kc, vc, kd, vd, cu)
+    mk = lambda *s_: torch.randn(*s_, device=dev, generator=g, dtype=torch.float32).to(dt)
+    qc, kc, vc, doc = mk(p, h, d), mk(p, hk, d), mk(p, hk, d), mk(p, h, d)
+    qb, kb, vb, dob = mk(tmax, h, d), mk(tmax, hk, d), mk(tmax, hk, d), mk(tmax, h, d)
+    groups = []
+    for rl in my_r:
+        t = sum(rl)
+        cu = np.concatenate([[0], np.cumsum(rl)]).astype(np.int64)
+        groups.append((dkv.DualKVInput(qb[:t], kc, vc, kb[:t], vb[:t], cu), dob[:t]))
 
     def step():
-        # Call 1 + Call 2 fused: one forward launch, one backward launch (prompt grads cast once)
-        oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc, dec)
-        return dkv.dualkv_two_call_bwd(qc, dec, oc, lc, doc, od, ld, dod, deterministic=False)
-
-    def step_separate():
-        # the reference's two separate calls (layer.py:243-255, 274-275), for comparison
-        oc, lc = dkv.fa2_varlen_fwd(ctx_b)
-        od, ld = dkv.dualkv_fwd(dec)
-        dkv.dualkv_bwd(dec, od, ld, dod, deterministic=False)
-        dkv.fa2_varlen_bwd(ctx_b, oc, lc, doc)
+        # per group: Call 1 + Call 2 fused -- one forward launch, one backward launch
+        for dec, dod in groups:
+            oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc, dec)
+            dkv.dualkv_two_call_bwd(qc, dec, oc, lc, doc, od, ld, dod, deterministic=False)
 
     def barrier():
         if world > 1:
@@ -244,89 +279,105 @@ def main():
             fn()
         e1.record()
         barrier()
-        ms = e0.elapsed_time(e1) / steps
+        ms_ = e0.elapsed_time(e1) / steps
         if world > 1:
-            tt = torch.tensor([ms], device=dev)
+            tt = torch.tensor([ms_], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms = tt.item()
-        return ms
+            ms_ = tt.item()
+        return ms_
 
     clocks = ClockSampler()
     clocks.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    # ---- headline: device-resident inputs, K steps, with per-kernel events from libdkv
+    # ---- headline: device-resident inputs, K steps, per-kernel CUDA events recorded by libdkv
     lib.dkv_profile_begin()
     ms = timed(step, args.steps)
     fms, fl, bms, bl, al = (ctypes.c_double(), ctypes.c_int32(), ctypes.c_double(), ctypes.c_int32(),
                             ctypes.c_int32())
     lib.dkv_profile_end(ctypes.byref(fms), ctypes.byref(fl), ctypes.byref(bms), ctypes.byref(bl),
                         ctypes.byref(al))
-    # fwd / bwd split (separately timed passes)
+    value = fl_job / (ms * 1e-3) / 1e12
+
+    # ---- first group: fwd / bwd split, separate-call comparison, replicated N-copy baseline, e2e
+    dec0, dod0 = groups[0]
+    rl0 = my_r[0]
+    pairs0 = visible_pairs(p, rl0, "dualkv")
     saved = {}
 
     def fwd_only():
-        saved["oc"], saved["lc"], saved["od"], saved["ld"] = dkv.dualkv_two_call_fwd(qc, dec)
+        saved["oc"], saved["lc"], saved["od"], saved["ld"] = dkv.dualkv_two_call_fwd(qc, dec0)
 
     fwd_ms = timed(fwd_only, args.steps)
 
     def bwd_only():
-        dkv.dualkv_two_call_bwd(qc, dec, saved["oc"], saved["lc"], doc, saved["od"], saved["ld"], dod,
+        dkv.dualkv_two_call_bwd(qc, dec0, saved["oc"], saved["lc"], doc, saved["od"], saved["ld"], dod0,
                                 deterministic=False)
 
     bwd_ms = timed(bwd_only, args.steps)
-    sep_ms = timed(step_separate, args.steps)
-    fl_step = flops_fwdbwd(c)
-    value = fl_step * world / (ms * 1e-3) / 1e12
+    ctx_b = dkv.VarlenBatch(qc, kc, vc, np.array([0, p]))
 
-    # ---- replicated N-copy baseline: same kernels over the N(P+R) layout
+    def step_separate():
+        # the reference's two separate calls (layer.py:243-255, 274-275), for comparison
+        oc, lc = dkv.fa2_varlen_fwd(ctx_b)
+        od, ld = dkv.dualkv_fwd(dec0)
+        dkv.dualkv_bwd(dec0, od, ld, dod0, deterministic=False)
+        dkv.fa2_varlen_bwd(ctx_b, oc, lc, doc)
+
+    sep_ms = timed(step_separate, args.steps)
+
     rep = None
     if not args.no_replicated:
-        s = p + r
-        qr, kr, vr, dor = mk(n * s, h, d), mk(n * s, hk, d), mk(n * s, hk, d), mk(n * s, h, d)
-        rb = dkv.VarlenBatch(qr, kr, vr, np.arange(0, n * s + 1, s, dtype=np.int64))
+        s_cu = np.concatenate([[0], np.cumsum([p + r for r in rl0])]).astype(np.int64)
+        ts = int(s_cu[-1])
+        qr, kr, vr, dor = mk(ts, h, d), mk(ts, hk, d), mk(ts, hk, d), mk(ts, h, d)
+        rb = dkv.VarlenBatch(qr, kr, vr, s_cu)
 
         def rep_step():
-            o, l = dkv.fa2_varlen_fwd(rb)
-            dkv.fa2_varlen_bwd(rb, o, l, dor)
+            o, l_ = dkv.fa2_varlen_fwd(rb)
+            dkv.fa2_varlen_bwd(rb, o, l_, dor)
 
         rep_step()
         rep_ms = timed(rep_step, max(1, min(args.steps, 3)))
-        rep = {"ms_per_step": round(rep_ms, 3),
-               "tflops_algorithmic": round(rep_flops_fwdbwd(c) / (rep_ms * 1e-3) / 1e12, 2),
-               "speedup_dualkv_vs_ncopy": round(rep_ms / ms, 3)}
+        grp_ms = fwd_ms + bwd_ms
+        rep = {"ms_per_group": round(rep_ms, 3),
+               "tflops_algorithmic": round(14 * visible_pairs(p, rl0, "standard") * h * d / (rep_ms * 1e-3) / 1e12, 2),
+               "dualkv_ms_per_group": round(grp_ms, 3),
+               "speedup_dualkv_vs_ncopy": round(rep_ms / grp_ms, 3),
+               "pair_ratio": round(visible_pairs(p, rl0, "standard") / pairs0, 3)}
         del qr, kr, vr, dor, rb
 
-    # ---- e2e: public API with pinned host buffers, H2D inputs + D2H outputs per step
     e2e = None
     if not args.no_e2e:
+        t0 = sum(rl0)
+        cu0 = np.concatenate([[0], np.cumsum(rl0)]).astype(np.int64)
         host_in = {k: v.cpu().pin_memory() for k, v in
-                   dict(qc=qc, kc=kc, vc=vc, q=q, kd=kd, vd=vd, doc=doc, dod=dod).items()}
-        out_shapes = [(p, h, d), (t, h, d), (t, h, d), (p, hk, d), (p, hk, d), (t, hk, d), (t, hk, d),
+                   dict(qc=qc, kc=kc, vc=vc, q=qb[:t0], kd=kb[:t0], vd=vb[:t0], doc=doc, dod=dob[:t0]).items()}
+        out_shapes = [(p, h, d), (t0, h, d), (t0, h, d), (p, hk, d), (p, hk, d), (t0, hk, d), (t0, hk, d),
                       (p, h, d)]
-        host_out = [torch.empty(s_, dtype=torch.bfloat16).pin_memory() for s_ in out_shapes]
+        host_out = [torch.empty(s_, dtype=dt).pin_memory() for s_ in out_shapes]
         h2d = sum(x.numel() * x.element_size() for x in host_in.values())
         d2h = sum(x.numel() * x.element_size() for x in host_out)
 
         def e2e_step():
             dv_ = {k: v.to(dev, non_blocking=True) for k, v in host_in.items()}
-            di = dkv.DualKVInput(dv_["q"], dv_["kc"], dv_["vc"], dv_["kd"], dv_["vd"], cu)
+            di = dkv.DualKVInput(dv_["q"], dv_["kc"], dv_["vc"], dv_["kd"], dv_["vd"], cu0)
             oc, lc, od, ld = dkv.dualkv_two_call_fwd(dv_["qc"], di)
             cq, gkc, gvc, gq, gkd, gvd = dkv.dualkv_two_call_bwd(dv_["qc"], di, oc, lc, dv_["doc"], od, ld,
                                                                  dv_["dod"], deterministic=False)
-            # every output of the layer's attention: both O's and all six input gradients
-            outs = [oc, od, gq, gkc, gvc, gkd, gvd, cq]
-            for ho, o in zip(host_out, outs):
+            # every output of the group's attention: both O's and all six input gradients
+            for ho, o in zip(host_out, [oc, od, gq, gkc, gvc, gkd, gvd, cq]):
                 ho.copy_(o, non_blocking=True)
 
         e2e_step()
         e2e_ms = timed(e2e_step, args.steps)
-        e2e = {"value": round(fl_step * world / (e2e_ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
-               "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+        e2e = {"value": round(14 * pairs0 * h * d * world / (e2e_ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+               "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "what": "one prompt group per GPU through the public API, pinned host buffers"}
     clk = clocks.stop()
 
-    # ---- roofline of the dominant kernel (backward main kernel of Call 2 + Call 1)
+    # ---- roofline of the dominant kernel (the backward main kernel)
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -334,21 +385,18 @@ def main():
     except Exception:
         pass
     peak_burst = peaks.get("bf16_tflops", 1590.0)
-    # per step each main kernel launches once (Call 1 fused into the Call 2 launch); achieved =
-    # algorithmic FLOPs / device time of that launch (CUDA events recorded around it by libdkv)
-    launches_per_step = 1
-    bwd_kernel_ms = bms.value / max(1, bl.value)
-    fwd_kernel_ms = fms.value / max(1, fl.value)
-    bwd_flops_per_launch = 10 * pairs(p, [r] * n) * h * d / launches_per_step
-    fwd_flops_per_launch = 4 * pairs(p, [r] * n) * h * d / launches_per_step
-    bwd_ach = bwd_flops_per_launch / (bwd_kernel_ms * 1e-3) / 1e12
-    fwd_ach = fwd_flops_per_launch / (fwd_kernel_ms * 1e-3) / 1e12
+    # per step and group each main kernel launches once (Call 1 fused into Call 2's launch):
+    # achieved = algorithmic FLOPs of those launches / their device time (CUDA events by libdkv)
+    bwd_ach = 10 * pairs_rank * h * d * args.steps / (bms.value * 1e-3) / 1e12 if bms.value else 0.0
+    fwd_ach = 4 * pairs_rank * h * d * args.steps / (fms.value * 1e-3) / 1e12 if fms.value else 0.0
     roof = {"bound": "tensor", "kernel": "dualkv_bwd_kernel (tcgen05; Call 1 fused into the Call 2 launch)",
             "achieved": round(bwd_ach, 2), "peak": peak_burst, "unit": "TFLOP/s",
             "frac": round(bwd_ach / peak_burst, 4), "traffic": None,
             "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "fallback 1.59 PF",
+            "algorithmic_per_launch": "10 * visible_pairs * H * d (SURVEY 8d)",
             "fwd_kernel": {"achieved": round(fwd_ach, 2), "frac": round(fwd_ach / peak_burst, 4)},
-            "kernel_ms": {"fwd_main_avg": round(fwd_kernel_ms, 4), "bwd_main_avg": round(bwd_kernel_ms, 4),
+            "kernel_ms": {"fwd_main_per_launch": round(fms.value / max(1, fl.value), 4),
+                          "bwd_main_per_launch": round(bms.value / max(1, bl.value), 4),
                           "fwd_main_share": round(fms.value / (ms * args.steps), 3),
                           "bwd_main_share": round(bms.value / (ms * args.steps), 3)}}
 
@@ -362,18 +410,19 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (randn, bf16)",
-            "config": {"workload": "C3: Qwen3-8B attention, one prompt group per GPU",
-                       "N": n, "P": p, "R": r, "H": h, "H_k": hk, "d": d,
-                       "global_groups": world, "parallelism": f"dp{world} over prompt groups",
-                       "l2": "inputs larger than L2 (q alone 512 MiB > 126 MB)",
+            "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None,
+            "dtype": cfg["dtype"], "data": "synthetic (randn)",
+            "config": {"workload": cfg["desc"], "N": cfg["n"], "P": p,
+                       "R": cfg["r"] if cfg["r"] != "ragged" else "U[512,4096]",
+                       "H": h, "H_k": hk, "d": d, "groups_this_rank": len(my_r),
+                       "parallelism": f"dp{world} over prompt groups",
+                       "l2": "inputs larger than L2" if tmax * h * d * 2 > 126e6 else "inputs may fit in L2",
                        "unit_of_work": "Call1+Call2 fwd+bwd (reference run_bench dk unit), fused two-call launches",
-                       "flops_per_group": fl_step},
-            "fwd_ms": round(fwd_ms, 3), "bwd_ms": round(bwd_ms, 3),
-            "separate_calls_ms_per_step": round(sep_ms, 3),
-            "fwd_tflops": round(4 * pairs(p, [r] * n) * h * d / (fwd_ms * 1e-3) / 1e12, 2),
-            "bwd_tflops": round(10 * pairs(p, [r] * n) * h * d / (bwd_ms * 1e-3) / 1e12, 2),
+                       "flops_per_step_job": fl_job},
+            "fwd_ms_group0": round(fwd_ms, 3), "bwd_ms_group0": round(bwd_ms, 3),
+            "fwd_tflops": round(4 * pairs0 * h * d / (fwd_ms * 1e-3) / 1e12, 2),
+            "bwd_tflops": round(10 * pairs0 * h * d / (bwd_ms * 1e-3) / 1e12, 2),
+            "separate_calls_ms_group0": round(sep_ms, 3),
             "replicated_ncopy": rep, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
             "gpu_launches": int(al.value), "clocks": clk,
         }
