@@ -28,8 +28,7 @@
 //   dK  += dS^T Q     (M128 N128 K64)   TS-MMA, A = dS^T (TMEM) -> TMEM [384,512)
 //   dQ^T = K^T dS^T   (M128 N64  K128)  SS-MMA                  -> TMEM [192,256)
 // Roles: warps 0-3 compute (thread = key row), 4-7 dQ drain (thread = head-dim
-// lane) + dV epilogue, 8 TMA producer + TMEM allocator, 9 MMA issuer, 10-11 idle
-// (setmaxnreg moves their registers to the compute / drain warpgroups).
+// lane) + dV epilogue, 8 TMA producer + TMEM allocator, 9 MMA issuer.
 #include "dkv_internal.h"
 #include "tma_host.h"
 
@@ -41,7 +40,7 @@ namespace bwd {
 constexpr int kBK = 128;  // keys per tile (MMA M)
 constexpr int kBQ = 64;   // query rows per tile (MMA N for S^T / dP^T / dQ^T)
 constexpr int D = 128;
-constexpr int kThreads = 384;  // 3 warpgroups: compute, dQ drain, producer/MMA (+2 idle warps)
+constexpr int kThreads = 320;
 constexpr int kStages = 3;
 constexpr int kKVBytes = kBK * D * 2;       // 32 KB
 constexpr int kKVPanel = kBK * 128;         // 16 KB
@@ -224,11 +223,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
   tc_fence_after();
   const uint32_t tmem = bar.tmem_base;
   const int G = p.group;
-  // registers: the producer/MMA warpgroup needs few, the compute and drain warpgroups many
-  if (warp >= 8)
-    regs_dec<40>();
-  else
-    regs_inc<232>();
 
   if (warp == 8) {
     // ================= producer: K/V once, then (Q, dO, lse/D) per query tile
