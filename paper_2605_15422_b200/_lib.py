@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdkv.so")
+# DKV_LIB: an alternative in-tree build (A/B timing of kernel variants); default libdkv.so
+LIB_PATH = os.path.join(_HERE, os.environ.get("DKV_LIB", "libdkv.so"))
 
 DKV_OK, DKV_ERR_INVALID, DKV_ERR_UNSUPPORTED, DKV_ERR_CUDA, DKV_ERR_WORKSPACE = 0, -1, -2, -3, -4
 DKV_BF16, DKV_F32 = 0, 1

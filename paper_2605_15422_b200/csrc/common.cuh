@@ -60,6 +60,28 @@ DKV_DEVICE float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// 3-input max (FMNMX3 on sm_100): halves the row-max instruction count
+DKV_DEVICE float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// Two 2^x on the FMA/ALU pipes with packed f32x2 arithmetic (FADD2/FFMA2): same algorithm as
+// ex2_poly, half the FMA-pipe instructions per exponential.
+DKV_DEVICE float2 ex2_poly2(float2 x) {
+  const float2 big = make_float2(12582912.f, 12582912.f);
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 t = __fadd2_rn(x, big);
+  const float2 f = __fadd2_rn(x, __fadd2_rn(big, make_float2(-t.x, -t.y)));
+  float2 p = __ffma2_rn(make_float2(0.05517025f, 0.05517025f), f, make_float2(0.24260791f, 0.24260791f));
+  p = __ffma2_rn(p, f, make_float2(0.69326091f, 0.69326091f));
+  p = __ffma2_rn(p, f, make_float2(0.99992830f, 0.99992830f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 DKV_DEVICE uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);

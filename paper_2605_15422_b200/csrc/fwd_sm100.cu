@@ -34,6 +34,7 @@ constexpr int kBM = 128;  // rows per Q tile
 constexpr int kBN = 128;  // keys per KV tile
 constexpr int kThreads = 320;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr int kPolyPairs = 5;              // of every 16 exponential pairs, on the FMA pipe
 
 template <int D>
 struct Cfg {
@@ -286,17 +287,14 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
           for (int c = 0; c < kBN; ++c)
             if (c > lim) s[c] = -INFINITY;
         }
-        // row max: 8 independent chains + a 3-level tree (a single 128-long dependent chain
-        // of FMNMX would sit on the softmax critical path)
-        float m8[8];
+        // row max: 4 independent chains of 3-input max (FMNMX3) + a short tree (one 128-long
+        // dependent chain would sit on the softmax critical path)
+        float m4[4] = {s[0], s[1], s[2], s[3]};
 #pragma unroll
-        for (int i = 0; i < 8; ++i) m8[i] = s[i];
+        for (int c = 4; c < kBN; c += 8)
 #pragma unroll
-        for (int c = 8; c < kBN; c += 8)
-#pragma unroll
-          for (int i = 0; i < 8; ++i) m8[i] = fmaxf(m8[i], s[c + i]);
-        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+          for (int i = 0; i < 4; ++i) m4[i] = fmax3(m4[i], s[c + 2 * i], s[c + 2 * i + 1]);
+        const float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
         const float m_tile = mx * p.scale_log2;
         const float m_new = fmaxf(m_run, m_tile);
         float alpha = 1.f;
@@ -305,23 +303,31 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
           m_run = m_new;
         }
         const float m_use = m_run == -INFINITY ? 0.f : m_run;
-        float rs[4] = {0.f, 0.f, 0.f, 0.f};
+        // x = s * scale * log2(e) - m in packed f32x2 (FFMA2), then 2^x: kPolyPairs of every
+        // 16 pairs on the FMA pipe (polynomial, f32x2) to unload the MUFU pipe; row sum in FADD2
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        const float2 nm2 = make_float2(-m_use, -m_use);
+        float2 rs2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int c0 = 0; c0 < kBN; c0 += 32) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float x0 = fmaf(s[c0 + 2 * i], p.scale_log2, -m_use);
-            const float x1 = fmaf(s[c0 + 2 * i + 1], p.scale_log2, -m_use);
-            // 1 in 4 exponentials on the FMA pipe (polynomial) to unload the MUFU pipe
-            const float e0 = i >= 12 ? ex2_poly(x0) : ex2(x0);
-            const float e1 = i >= 12 ? ex2_poly(x1) : ex2(x1);
-            rs[i & 3] += e0 + e1;
-            pk[i] = pack_bf16(e0, e1);
+            const float2 x = __ffma2_rn(make_float2(s[c0 + 2 * i], s[c0 + 2 * i + 1]), sc2, nm2);
+            float2 e;
+            if (i >= 16 - kPolyPairs) {
+              e = ex2_poly2(x);
+            } else {
+              e.x = ex2(x.x);
+              e.y = ex2(x.y);
+            }
+            rs2[i & 1] = __fadd2_rn(rs2[i & 1], e);
+            pk[i] = pack_bf16(e.x, e.y);
           }
           tmem_st16(tS + c0 / 2, pk);
         }
-        const float rowsum = (rs[0] + rs[1]) + (rs[2] + rs[3]);
+        const float2 rsum = __fadd2_rn(rs2[0], rs2[1]);
+        const float rowsum = rsum.x + rsum.y;
         l_run = l_run * alpha + rowsum;
         // O holds P V of iterations < it (its MMA completed before S(it) did)
         if (it > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
@@ -330,8 +336,13 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
             uint32_t r[32];
             tmem_ld32(tO + c0, r);
             tmem_wait_ld();
+            const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            for (int i = 0; i < 32; i += 2) {
+              const float2 v = __fmul2_rn(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), a2);
+              r[i] = __float_as_uint(v.x);
+              r[i + 1] = __float_as_uint(v.y);
+            }
             tmem_st32(tO + c0, r);
           }
         }

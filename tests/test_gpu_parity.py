@@ -140,13 +140,17 @@ def test_fwd_bwd_bf16_vs_f64_and_replicated(case, cuda_device):
     ours = [o] + list(g)
     names = ("O", "dQ", "dK_c", "dV_c", "dK_d", "dV_d")
     toy = sum(rl) * (p + 1) < 64
+    # toy shapes (a query sees one or two keys): dS = P (dP - D) with P ~ 1/2 cancels, so a
+    # one-ulp flip in the bf16 O behind D moves a gradient by ~1 % of max|ref| -- the two
+    # layouts round O differently; the slack there is 2e-2 max|ref| instead of 2e-3
+    slack = 2e-2 if toy else 2e-3
     for got, r_out, ref, name in zip(ours, rep, [o64] + list(g64), names):
         if ref.size == 0:
             continue
         e_dk = np.max(np.abs(to_np(got) - ref))
         e_rep = np.max(np.abs(r_out - ref))
         scale = max(np.max(np.abs(ref)), 1e-30)
-        assert e_dk <= 2 * e_rep + 2e-3 * scale, \
+        assert e_dk <= 2 * e_rep + slack * scale, \
             f"{name}: DualKV err {e_dk:.3e} vs replicated {e_rep:.3e} (max|ref| {scale:.3e})"
         if not toy:
             rel = e_dk / max(np.max(np.abs(ref)), 1e-30)

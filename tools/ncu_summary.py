@@ -20,6 +20,11 @@ METRICS = [
     ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem wavefronts from tensor core %"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem wavefronts from LSU %"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),
+    ("lts__t_bytes.sum", "L2 bytes (all ops)"),
+    ("lts__t_sectors_op_red.sum", "L2 sectors, reductions (red / TMA reduce-add)"),
+    ("lts__t_sectors_op_atom.sum", "L2 sectors, atomics"),
+    ("lts__t_sectors_op_read.sum", "L2 sectors, reads"),
+    ("lts__t_sectors_op_write.sum", "L2 sectors, writes"),
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),

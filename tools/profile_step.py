@@ -1,7 +1,9 @@
-"""One C3 DualKV step (Call 1 + Call 2, fwd + bwd) for ncu captures.
+"""One C3 DualKV step (Call 1 + Call 2 fused, fwd + bwd -- what bench.py times) for ncu captures.
 
     ncu --set full --clock-control none --import-source on -k regex:dualkv_bwd -c 1 \
         -o gpurun_out/prof python tools/profile_step.py
+    python tools/profile_step.py small      # N=8 P=2K R=512
+    SEPARATE=1 python tools/profile_step.py # the reference's two separate calls
 """
 
 import os
@@ -25,9 +27,13 @@ q, kd, vd, dod = mk(t, h, d), mk(t, hk, d), mk(t, hk, d), mk(t, h, d)
 ctx = dkv.VarlenBatch(qc, kc, vc, np.array([0, p]))
 dec = dkv.DualKVInput(q, kc, vc, kd, vd, np.arange(0, t + 1, r))
 for _ in range(steps):
-    oc, lc = dkv.fa2_varlen_fwd(ctx)
-    od, ld = dkv.dualkv_fwd(dec)
-    dkv.dualkv_bwd(dec, od, ld, dod, deterministic=False)
-    dkv.fa2_varlen_bwd(ctx, oc, lc, doc)
+    if os.environ.get("SEPARATE"):
+        oc, lc = dkv.fa2_varlen_fwd(ctx)
+        od, ld = dkv.dualkv_fwd(dec)
+        dkv.dualkv_bwd(dec, od, ld, dod, deterministic=False)
+        dkv.fa2_varlen_bwd(ctx, oc, lc, doc)
+    else:
+        oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc, dec)
+        dkv.dualkv_two_call_bwd(qc, dec, oc, lc, doc, od, ld, dod, deterministic=False)
 torch.cuda.synchronize()
 print("done")
