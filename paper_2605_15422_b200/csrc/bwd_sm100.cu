@@ -492,14 +492,29 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
 
 }  // namespace bwd
 
-bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads) {
-  if (dtype != DKV_BF16 || head_dim != bwd::D || force_simt()) return false;
-  if (kv_heads <= 0 || heads % kv_heads) return false;
+// DKV_BWD_V2=1: bwd2_sm100.cu's 128x128-tile kernel instead of the 64-row one below (experimental:
+// same speed today, and its dS uses the bf16-rounded P -- see DESIGN.md §4.2c)
+static bool use_v1() {
+  static const bool v = [] {
+    const char* e = getenv("DKV_BWD_V2");
+    return !(e && e[0] == '1');
+  }();
+  return v;
+}
+
+static bool tc_bwd1_supported(int head_dim, int heads, int kv_heads) {
+  if (head_dim != bwd::D || kv_heads <= 0 || heads % kv_heads) return false;
   const int G = heads / kv_heads;
   return G <= bwd::kBQ && (bwd::kBQ % G) == 0;
 }
 
+bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads) {
+  if (dtype != DKV_BF16 || force_simt()) return false;
+  return use_v1() ? tc_bwd1_supported(head_dim, heads, kv_heads) : tc_bwd2_supported(head_dim, heads, kv_heads);
+}
+
 int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, cudaStream_t st) {
+  if (!use_v1()) return launch_tc_bwd2(a, self, w, st);
   using namespace bwd;
   Params p{};
   const int G = a.heads / a.kv_heads;

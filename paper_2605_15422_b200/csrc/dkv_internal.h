@@ -85,5 +85,8 @@ struct BwdScratch {
   bool atomic_ctx;
 };
 int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, cudaStream_t st);
+// bwd2_sm100.cu: the 128x128-tile backward (experimental, DKV_BWD_V2=1)
+bool tc_bwd2_supported(int head_dim, int heads, int kv_heads);
+int launch_tc_bwd2(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, cudaStream_t st);
 
 }  // namespace dkv

@@ -4,7 +4,7 @@ import os
 import subprocess
 import sys
 
-if len(sys.argv) > 1:
+if len(sys.argv) > 1 and sys.argv[1] == "run":
     import numpy as np
     import torch
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -29,5 +29,5 @@ if len(sys.argv) > 1:
     torch.cuda.synchronize()
     print(f"ablate={os.environ.get('DKV_BWD_ABLATE', '0')} bwd_ms={e0.elapsed_time(e1) / 5:.3f}", flush=True)
 else:
-    for a in ("0", "1", "2", "4", "3", "7"):
+    for a in (sys.argv[1:] or ["0", "1", "2", "4", "3", "7"]):
         subprocess.run([sys.executable, __file__, "run"], env={**os.environ, "DKV_BWD_ABLATE": a})

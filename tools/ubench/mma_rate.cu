@@ -17,7 +17,7 @@ __device__ uint64_t kdesc(uint32_t saddr, int sw) {
   return d;
 }
 
-struct Cfg { int ts, n, sw_a, sw_b, b_mn; };
+struct Cfg { int ts, n, sw_a, sw_b, b_mn, a_mn; };
 
 __global__ void __launch_bounds__(128, 1) k_rate(Cfg c, int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -34,13 +34,13 @@ __global__ void __launch_bounds__(128, 1) k_rate(Cfg c, int iters, unsigned long
   const uint32_t tmem = tbase;
   if (threadIdx.x < 32 && elect_one()) {
     const uint32_t a = smem_u32(base), b = smem_u32(base + 65536);
-    const uint32_t id = idesc_bf16_f32(128, c.n, false, c.b_mn != 0);
+    const uint32_t id = idesc_bf16_f32(128, c.n, c.a_mn != 0, c.b_mn != 0);
     uint64_t ad[8], bd[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int kpa = c.sw_a / 32, kpb = c.sw_b / 32;  // K steps per swizzle row
       const uint32_t aoff = c.ts ? 0 : (k / kpa) * (128 * c.sw_a) + (k % kpa) * 32;
-      ad[k] = c.ts ? 0 : kdesc(a + aoff, c.sw_a);
+      ad[k] = c.ts ? 0 : c.a_mn ? sdesc_sw128(a + k * 2048, 16384, 1024) : kdesc(a + aoff, c.sw_a);
       if (c.b_mn) {
         bd[k] = sdesc_sw128(b + k * 2048, 64 * 128 * 2 /*LBO: next 64-wide MN atom*/, 1024);
       } else {
@@ -72,14 +72,8 @@ int main() {
   unsigned long long* d; cudaMalloc(&d, 64);
   cudaFuncSetAttribute(k_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   Cfg cfgs[] = {
-    {0, 64, 128, 128, 0}, {0, 128, 128, 128, 0}, {0, 256, 128, 128, 0},
-    {0, 64, 64, 64, 0}, {0, 128, 64, 64, 0}, {0, 256, 64, 64, 0},
-    {0, 64, 32, 32, 0}, {0, 128, 32, 32, 0}, {0, 256, 32, 32, 0},
-    {0, 64, 32, 128, 0}, {0, 128, 32, 128, 0}, {0, 64, 128, 32, 0}, {0, 128, 128, 32, 0},
-    {0, 64, 128, 128, 1}, {0, 128, 128, 128, 1}, {0, 64, 32, 128, 1}, {0, 128, 32, 128, 1},
-    {1, 64, 0, 128, 0}, {1, 128, 0, 128, 0}, {1, 256, 0, 128, 0},
-    {1, 64, 0, 32, 0}, {1, 128, 0, 32, 0}, {1, 256, 0, 32, 0},
-    {1, 64, 0, 128, 1}, {1, 128, 0, 128, 1},
+    {0, 128, 128, 128, 0, 0}, {0, 128, 128, 128, 1, 0}, {0, 128, 128, 128, 1, 1}, {0, 128, 128, 128, 0, 1},
+    {0, 64, 128, 128, 1, 1}, {1, 128, 0, 128, 1, 0}, {1, 128, 0, 128, 0, 0}, {0, 128, 32, 32, 0, 0},
   };
   for (auto c : cfgs) {
     float best = 1e9; unsigned long long clk = 0;
@@ -95,8 +89,8 @@ int main() {
       if (ms < best) best = ms;
     }
     double flop = 2.0 * 128 * c.n * 16 * 8192 * 148;
-    printf("%s N%-3d A:%s B:%s%-4s clk/mma %6.1f ideal %3d  %5.0f TFLOP/s\n", c.ts ? "TS" : "SS", c.n,
-           c.ts ? "tmem " : (c.sw_a == 128 ? "sw128" : c.sw_a == 64 ? "sw64 " : "sw32 "),
+    printf("%s N%-3d A%s:%s B:%s%-4s clk/mma %6.1f ideal %3d  %5.0f TFLOP/s\n", c.ts ? "TS" : "SS", c.n,
+           c.a_mn ? "(MN)" : "", c.ts ? "tmem " : (c.sw_a == 128 ? "sw128" : c.sw_a == 64 ? "sw64 " : "sw32 "),
            c.sw_b == 128 ? "sw128" : c.sw_b == 64 ? "sw64 " : "sw32 ", c.b_mn ? "(MN)" : "", (double)clk / 8192,
            128 * c.n / 256, flop / (best * 1e-3) / 1e12);
   }
