@@ -70,8 +70,26 @@ def _offsets(cu, total: int, what: str) -> Tuple[np.ndarray, torch.Tensor]:
     if np.any(np.diff(host) < 0):
         raise ValueError(f"{what} must be non-decreasing")
     if dev is None or dev.dtype != torch.int32:
-        dev = torch.as_tensor(host.astype(np.int32), device="cuda")
+        dev = _device_offsets(host)
     return host, dev.contiguous()
+
+
+_CU_CACHE: dict = {}
+
+
+def _device_offsets(host: np.ndarray) -> torch.Tensor:
+    """int32 device copy of host offsets, cached by content: the first use pays one synchronous
+    copy, every later call with the same offsets (every training step of a fixed layout) enqueues
+    nothing -- a per-call pageable copy would block the host on the current stream."""
+    key = (torch.cuda.current_device(), host.tobytes())
+    dev = _CU_CACHE.get(key)
+    if dev is None:
+        if len(_CU_CACHE) >= 256:  # rare: drop the cache once no kernel can still read it
+            torch.cuda.synchronize()
+            _CU_CACHE.clear()
+        dev = torch.as_tensor(host.astype(np.int32), device="cuda")
+        _CU_CACHE[key] = dev
+    return dev
 
 
 def uses_tensor_cores(dtype: torch.dtype, head_dim: int, heads: int, kv_heads: int) -> bool:

@@ -62,10 +62,64 @@ __global__ void rowsum_kernel(SimtArgs a, float* drow, __nv_bfloat16* xsplit, in
   }
 }
 
+// bf16 fast path: LPR = head_dim / 16 lanes per (token, head) row, two 16-byte loads of O and of
+// dO per lane (fully coalesced), a log2(LPR)-step shuffle reduction, one 64 B xsplit row store.
+template <int LPR>
+__global__ void rowsum_bf16_kernel(SimtArgs a, float* drow, __nv_bfloat16* xsplit, int tpad) {
+  const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int sub = threadIdx.x & (LPR - 1);
+  const int64_t row = gt / LPR;  // (t, h) row, t-major
+  const int rows = xsplit ? tpad : a.total_q;
+  const bool live = row < static_cast<int64_t>(rows) * a.heads;
+  const int t = live ? static_cast<int>(row / a.heads) : 0, h = live ? static_cast<int>(row % a.heads) : 0;
+  float acc = 0.f;
+  if (live && t < a.total_q) {
+    const int64_t off = row * (LPR * 16) + sub * 16;
+    const uint4* o = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.out) + off);
+    const uint4* g = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.dout) + off);
+    const uint4 o0 = o[0], o1 = o[1], g0 = g[0], g1 = g[1];
+    const uint32_t ov[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+    const uint32_t gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      acc = fmaf(__uint_as_float(ov[i] << 16), __uint_as_float(gv[i] << 16), acc);
+      acc = fmaf(__uint_as_float(ov[i] & 0xffff0000u), __uint_as_float(gv[i] & 0xffff0000u), acc);
+    }
+  }
+#pragma unroll
+  for (int s = LPR / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if (!live || sub != 0) return;
+  if (drow && t < a.total_q) drow[static_cast<int64_t>(h) * a.total_q + t] = acc;
+  if (xsplit) {
+    const int G = a.heads / a.kv_heads;
+    const int hk = h / G, gi = h % G;
+    __nv_bfloat16 v[32];
+    for (int i = 0; i < 32; ++i) v[i] = __float2bfloat16_rn(0.f);
+    if (t < a.total_q) {
+      const float lse = a.lse[static_cast<int64_t>(h) * a.total_q + t];
+      split3_bf16(-lse / a.scale, v[0], v[1], v[2]);
+      split3_bf16(-acc, v[16], v[17], v[18]);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(xsplit + ((static_cast<int64_t>(hk) * tpad + t) * G + gi) * 32);
+    const uint4* src = reinterpret_cast<const uint4*>(v);
+    for (int i = 0; i < 4; ++i) dst[i] = src[i];
+  }
+}
+
 void launch_rowsum_do_o(const SimtArgs& a, float* drow, __nv_bfloat16* xsplit, int tpad, cudaStream_t st) {
   const int64_t rows = xsplit ? tpad : a.total_q;
   const int64_t warps = rows * a.heads;
   if (warps == 0) return;
+  if (a.dtype == DKV_BF16 && (a.head_dim == 128 || a.head_dim == 64)) {
+    const int lpr = a.head_dim / 16;
+    const int threads = 256;
+    const int64_t blocks = (warps * lpr + threads - 1) / threads;
+    if (lpr == 8)
+      rowsum_bf16_kernel<8><<<blocks, threads, 0, st>>>(a, drow, xsplit, tpad);
+    else
+      rowsum_bf16_kernel<4><<<blocks, threads, 0, st>>>(a, drow, xsplit, tpad);
+    return;
+  }
   const int threads = 256;
   const int64_t blocks = (warps * 32 + threads - 1) / threads;
   if (a.dtype == DKV_F32)

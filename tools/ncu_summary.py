@@ -92,18 +92,18 @@ def launches(path: str) -> str:
         if r[i_m] != "gpu__time_duration.sum":
             continue
         v = float(r[i_v].replace(",", ""))
-        if r[i_u] == "usecond":
+        if r[i_u] in ("usecond", "us"):
             v /= 1e3
-        elif r[i_u] == "nsecond":
+        elif r[i_u] in ("nsecond", "ns"):
             v /= 1e6
         name = r[i_k].split("(")[0][:60]
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += v
     tot = sum(v for _, v in agg.values()) or 1.0
-    out = ["| kernel | launches | total ms | share |", "|---|---|---|---|"]
+    out = ["| kernel | launches | total ms | ms per launch | share |", "|---|---|---|---|---|"]
     for k, (n, ms) in sorted(agg.items(), key=lambda x: -x[1][1]):
-        out.append(f"| `{k}` | {n} | {ms:.3f} | {ms / tot:.1%} |")
+        out.append(f"| `{k}` | {n} | {ms:.3f} | {ms / n:.4f} | {ms / tot:.1%} |")
     return "\n".join(out) + "\n"
 
 
