@@ -32,6 +32,7 @@
 // tiles from the sequence end down so all key tiles of a sequence move in lockstep).
 #include "dkv_internal.h"
 #include "tma_host.h"
+#include "trace.cuh"
 
 #include <cstdlib>
 
@@ -125,25 +126,6 @@ struct QIter {
     }
   }
 };
-
-// -DDKV_TRACE builds (tools/trace_bwd.py): per-event clock64 timestamps of one CTA's first
-// kTraceTiles query tiles, read back with dkv_trace_read.  Compiled out otherwise.
-#ifdef DKV_TRACE
-constexpr int kTraceTiles = 256;
-constexpr int kTraceEvents = 16;
-__device__ long long g_trace[kTraceEvents * kTraceTiles];
-__device__ int g_trace_cta;
-#define TRACE(ev, i)                                                                   \
-  do {                                                                                 \
-    if (blockIdx.x == g_trace_cta && (i) < kTraceTiles) g_trace[(ev) * kTraceTiles + (i)] = clock64(); \
-  } while (0)
-#else
-#define TRACE(ev, i) \
-  do {               \
-  } while (0)
-#endif
-enum TraceEv { T_Q_LOAD, T_DO_LOAD, T_ISS_S, T_ISS_DP, T_ISS_DV, T_ISS_DK, T_ISS_DQ, T_C_S, T_C_P, T_C_DP, T_C_DS,
-               T_D_DQ, T_D_LD, T_D_END, T_MMA_END };
 
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
@@ -565,21 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd2_kernel(const __grid_c
 
 }  // namespace bwd2
 
-#ifdef DKV_TRACE
-extern "C" __attribute__((visibility("default"))) int dkv_trace_read(long long* dst, int cta) {
-  // cta >= 0: arm the trace for that CTA of the next launch (clears); cta < 0: copy it out
-  if (cta >= 0) {
-    static long long zeros[bwd2::kTraceEvents * bwd2::kTraceTiles] = {};
-    cudaMemcpyToSymbol(bwd2::g_trace, zeros, sizeof(zeros));
-    cudaMemcpyToSymbol(bwd2::g_trace_cta, &cta, sizeof(int));
-    return 0;
-  }
-  return cudaMemcpyFromSymbol(dst, bwd2::g_trace, sizeof(long long) * bwd2::kTraceEvents * bwd2::kTraceTiles) ==
-                 cudaSuccess
-             ? 0
-             : -1;
-}
-#endif
+DKV_TRACE_READ_FN(dkv_trace_read)
 
 bool tc_bwd2_supported(int head_dim, int heads, int kv_heads) {
   if (head_dim != bwd2::D || kv_heads <= 0 || heads % kv_heads) return false;

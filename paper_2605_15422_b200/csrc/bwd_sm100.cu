@@ -27,10 +27,14 @@
 //   dV  += P^T dO     (M128 N128 K64)   TS-MMA, A = P^T (TMEM)  -> TMEM [256,384)
 //   dK  += dS^T Q     (M128 N128 K64)   TS-MMA, A = dS^T (TMEM) -> TMEM [384,512)
 //   dQ^T = K^T dS^T   (M128 N64  K128)  SS-MMA                  -> TMEM [192,256)
-// Roles: warps 0-3 compute (thread = key row), 4-7 dQ drain (thread = head-dim
-// lane) + dV epilogue, 8 TMA producer + TMEM allocator, 9 MMA issuer.
+// Roles: warps 0-7 compute (thread = key row; two warps per TMEM lane quadrant,
+// 32 query columns each, so TMEM-load latency and MUFU work of one overlap the
+// other's; part of the exponentials on the FMA pipe), 8-11 dQ drain (thread =
+// head-dim lane), 12 TMA producer + TMEM allocator, 13 MMA issuer; warps 0-7
+// run the dK / dV epilogue.
 #include "dkv_internal.h"
 #include "tma_host.h"
+#include "trace.cuh"
 
 #include <cstdlib>
 
@@ -40,7 +44,10 @@ namespace bwd {
 constexpr int kBK = 128;  // keys per tile (MMA M)
 constexpr int kBQ = 64;   // query rows per tile (MMA N for S^T / dP^T / dQ^T)
 constexpr int D = 128;
-constexpr int kThreads = 320;
+constexpr int kThreads = 448;  // 8 compute warps, 4 dQ-drain warps, producer, MMA issuer
+constexpr int kWDrain = 8, kWProd = 12, kWMma = 13;
+constexpr int kDrainT0 = kWDrain * 32;  // first drain thread
+constexpr int kPolyPairs = 4;           // of every 16 exponential pairs, on the FMA pipe
 constexpr int kStages = 3;
 constexpr int kKVBytes = kBK * D * 2;       // 32 KB
 constexpr int kKVPanel = kBK * 128;         // 16 KB
@@ -195,8 +202,8 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
   if (threadIdx.x == 0) {
     mbar_init(&bar.kv_full, 1);
     mbar_init(&bar.sdp_full, 1);
-    mbar_init(&bar.sdp_empty, 128);
-    mbar_init(&bar.pds_full, 128);
+    mbar_init(&bar.sdp_empty, 256);
+    mbar_init(&bar.pds_full, 256);
     mbar_init(&bar.pds_empty, 1);
     mbar_init(&bar.kv_done, 1);
     for (int i = 0; i < kStages; ++i) {
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     mbar_init(&bar.dq_empty, 128);
     fence_mbar_init();
   }
-  if (warp == 8) tmem_alloc<512>(&bar.tmem_base);
+  if (warp == kWProd) tmem_alloc<512>(&bar.tmem_base);
   if (warp < 4) {
     // A operand of the additive-constant MMAs: row r = (1, 1, 1, 0, ..., 0) in SW32 K-major layout
     const int r = threadIdx.x;
@@ -224,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
   const uint32_t tmem = bar.tmem_base;
   const int G = p.group;
 
-  if (warp == 8) {
+  if (warp == kWProd) {
     // ================= producer: K/V once, then (Q, dO, lse/D) per query tile
     const CUtensorMap* mk = ctx_keys ? &p.tm_kc : &p.tm_k;
     const CUtensorMap* mv = ctx_keys ? &p.tm_vc : &p.tm_v;
@@ -248,6 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         const int st = i % kStages;
         const uint32_t ph = (i / kStages) & 1;
         mbar_wait(&bar.q_empty[st], ph ^ 1);
+        TRACE(T_Q_LOAD, i);
         const int row0 = cu[it.s] + it.tok;
         mbar_arrive_expect_tx(&bar.q_full[st], ((p.ablate & 4) ? 0 : 2 * kQBytes) + 2 * kXBytes);
         for (int pn = 0; pn < 2 && !(p.ablate & 4); ++pn) {
@@ -260,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         tma_load_2d(base + kOffX + st * 2 * kXBytes + kXBytes, mx, &bar.q_full[st], 16, xrow);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kWMma) {
     // ================= MMA issuer
     if (elect_one()) {
       const uint32_t tS = tmem, tdP = tmem + 64, tP = tmem + 128, tDS = tmem + 160, tdQ = tmem + 192;
@@ -268,9 +276,15 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       const uint32_t id_sdp = idesc_bf16_f32(kBK, kBQ, false, false);
       const uint32_t id_kv = idesc_bf16_f32(kBK, D, false, true);
       const uint32_t id_dq = idesc_bf16_f32(D, kBQ, true, true);
-      const uint32_t aK = smem_u32(base + kOffK), aV = smem_u32(base + kOffV);
-      const uint32_t aDS = smem_u32(base + kOffDS);
-      const uint32_t aOnes = smem_u32(base + kOffOnes), aX = smem_u32(base + kOffX);
+      // descriptors built once; a K step adds its byte offset >> 4 to the start-address field
+      const uint64_t dKk = sdesc_sw128(smem_u32(base + kOffK), 16, 1024);
+      const uint64_t dVk = sdesc_sw128(smem_u32(base + kOffV), 16, 1024);
+      const uint64_t dKt = sdesc_sw128(smem_u32(base + kOffK), kKVPanel, 1024);  // K^T, MN-major
+      const uint64_t dDS = sdesc_sw128(smem_u32(base + kOffDS), kPBytes, 1024);
+      const uint64_t dOnes = sdesc_sw32(smem_u32(base + kOffOnes));
+      auto koff_kv = [](int k) { return static_cast<uint64_t>(((k >> 2) * kKVPanel + (k & 3) * 32) >> 4); };
+      auto koff_q = [](int k) { return static_cast<uint64_t>(((k >> 2) * kQPanel + (k & 3) * 32) >> 4); };
+      auto koff_mn = [](int k) { return static_cast<uint64_t>((k * 2048) >> 4); };
       mbar_wait(&bar.kv_full, 0);
       for (int i = 0; i <= nq; ++i) {
         if (i < nq) {
@@ -278,56 +292,53 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
           mbar_wait(&bar.q_full[st], (i / kStages) & 1);
           if (i > 0) mbar_wait(&bar.sdp_empty, (i - 1) & 1);
           tc_fence_after();
-          const uint32_t aQ = smem_u32(base + kOffQ + st * kQBytes);
-          const uint32_t aDO = smem_u32(base + kOffDO + st * kQBytes);
+          const uint64_t dQk = sdesc_sw128(smem_u32(base + kOffQ + st * kQBytes), 16, 1024);
+          const uint64_t dOk = sdesc_sw128(smem_u32(base + kOffDO + st * kQBytes), 16, 1024);
+          const uint64_t dX = sdesc_sw32(smem_u32(base + kOffX + st * 2 * kXBytes));
+          TRACE(T_ISS_S, i);
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t oa = (k >> 2) * kKVPanel + (k & 3) * 32;
-            const uint32_t ob = (k >> 2) * kQPanel + (k & 3) * 32;
-            mma_ss(tS, sdesc_sw128(aK + oa, 16, 1024), sdesc_sw128(aQ + ob, 16, 1024), id_sdp, k > 0);
-          }
+          for (int k = 0; k < D / 16; ++k) mma_ss(tS, dKk + koff_kv(k), dQk + koff_q(k), id_sdp, k > 0);
           // S^T[k][c] += -lse[c] / scale  (so that P = exp2(S'^T * scale * log2 e))
-          mma_ss(tS, sdesc_sw32(aOnes), sdesc_sw32(aX + st * 2 * kXBytes), id_sdp, 1u);
+          mma_ss(tS, dOnes, dX, id_sdp, 1u);
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t oa = (k >> 2) * kKVPanel + (k & 3) * 32;
-            const uint32_t ob = (k >> 2) * kQPanel + (k & 3) * 32;
-            mma_ss(tdP, sdesc_sw128(aV + oa, 16, 1024), sdesc_sw128(aDO + ob, 16, 1024), id_sdp, k > 0);
-          }
+          for (int k = 0; k < D / 16; ++k) mma_ss(tdP, dVk + koff_kv(k), dOk + koff_q(k), id_sdp, k > 0);
           // dP^T[k][c] += -D[c]  (so that dS^T = P^T * dP'^T)
-          mma_ss(tdP, sdesc_sw32(aOnes), sdesc_sw32(aX + st * 2 * kXBytes + kXBytes), id_sdp, 1u);
+          mma_ss(tdP, dOnes, dX + (kXBytes >> 4), id_sdp, 1u);
           mma_commit(&bar.sdp_full);
         }
         if (i > 0) {
           const int j = i - 1;
           const int sj = j % kStages;
-          const uint32_t aQ = smem_u32(base + kOffQ + sj * kQBytes);
-          const uint32_t aDO = smem_u32(base + kOffDO + sj * kQBytes);
+          const uint64_t dQm = sdesc_sw128(smem_u32(base + kOffQ + sj * kQBytes), kQPanel, 1024);
+          const uint64_t dOm = sdesc_sw128(smem_u32(base + kOffDO + sj * kQBytes), kQPanel, 1024);
           mbar_wait(&bar.pds_full, j & 1);
           tc_fence_after();
+          TRACE(T_ISS_DV, j);
 #pragma unroll
           for (int k = 0; k < kBQ / 16; ++k)
-            mma_ts(tdV, tP + k * 8, sdesc_sw128(aDO + k * 2048, kQPanel, 1024), id_kv, (j > 0 || k > 0) ? 1u : 0u);
+            mma_ts(tdV, tP + k * 8, dOm + koff_mn(k), id_kv, (j > 0 || k > 0) ? 1u : 0u);
 #pragma unroll
           for (int k = 0; k < kBQ / 16; ++k)
-            mma_ts(tdK, tDS + k * 8, sdesc_sw128(aQ + k * 2048, kQPanel, 1024), id_kv, (j > 0 || k > 0) ? 1u : 0u);
+            mma_ts(tdK, tDS + k * 8, dQm + koff_mn(k), id_kv, (j > 0 || k > 0) ? 1u : 0u);
           mma_commit(&bar.q_empty[sj]);
           mbar_wait(&bar.dq_empty, (j & 1) ^ 1);
           tc_fence_after();
+          TRACE(T_ISS_DQ, j);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            mma_ss(tdQ, sdesc_sw128(aK + k * 2048, kKVPanel, 1024), sdesc_sw128(aDS + k * 2048, kPBytes, 1024),
-                   id_dq, k > 0);
+          for (int k = 0; k < kBK / 16; ++k) mma_ss(tdQ, dKt + koff_mn(k), dDS + koff_mn(k), id_dq, k > 0);
           mma_commit(&bar.dq_full);
           mma_commit(&bar.pds_empty);
         }
       }
       mma_commit(&bar.kv_done);
     }
-  } else if (warp < 4) {
-    // ================= compute WG: thread = key row r of the tile
-    const int r = warp * 32 + lane;
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+  } else if (warp < kWDrain) {
+    // ================= compute warps: thread = key row r of the tile, 32 query columns
+    // [c0, c0+32) per warp; two warps per TMEM lane quadrant so one's TMEM-load latency and
+    // MUFU work overlap the other's
+    const int r = (warp & 3) * 32 + lane;
+    const int c0 = (warp >> 2) * 32;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const int key = kbase + r;  // region-local key index
     uint8_t* sDS = base + kOffDS;
     QIter it;
@@ -337,12 +348,12 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       mbar_wait(&bar.q_full[st], (i / kStages) & 1);
       mbar_wait(&bar.sdp_full, i & 1);
       tc_fence_after();
-      uint32_t us[64], ud[64];
-      tmem_ld32(tmem + lane_off + 0, *reinterpret_cast<uint32_t(*)[32]>(&us[0]));
-      tmem_ld32(tmem + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(&us[32]));
-      tmem_ld32(tmem + lane_off + 64, *reinterpret_cast<uint32_t(*)[32]>(&ud[0]));
-      tmem_ld32(tmem + lane_off + 96, *reinterpret_cast<uint32_t(*)[32]>(&ud[32]));
+      if (threadIdx.x == 0) TRACE(T_C_S, i);
+      uint32_t us[32], ud[32];
+      tmem_ld32(tmem + lane_off + c0, us);
+      tmem_ld32(tmem + lane_off + 64 + c0, ud);
       tmem_wait_ld();
+      if (threadIdx.x == 0) TRACE(T_C_DP, i);
       tc_fence_before();
       mbar_arrive(&bar.sdp_empty);
       // key visible to query column c?  Visible columns form a range [cmin, cmax): context keys
@@ -357,84 +368,95 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         cmin = dt <= 0 ? 0 : min(dt * G, kBQ);
       }
       const int cmax = min(kBQ, (it.rlen - it.tok) * G);
-      const float sl2 = p.scale_log2;
-      uint32_t pp[32], pd[32];
+      const float2 sl2 = make_float2(p.scale_log2, p.scale_log2);
+      uint32_t pp[16], pd[16];
       // S' = S - lse/scale and dP' = dP - D arrive from the MMA: P = exp2(S' scale log2e),
       // dS = P dP' (the softmax scale is applied once to dK in the epilogue and dQ in its cast)
       if (p.ablate & 2) {
 #pragma unroll
-        for (int c2 = 0; c2 < 32; ++c2) {
+        for (int c2 = 0; c2 < 16; ++c2) {
           pp[c2] = us[2 * c2] ^ us[2 * c2 + 1];
           pd[c2] = ud[2 * c2] ^ ud[2 * c2 + 1];
         }
-      } else if (__all_sync(0xffffffffu, cmin == 0 && cmax == kBQ)) {
-#pragma unroll
-        for (int c2 = 0; c2 < 32; ++c2) {
-          const float e0 = ex2(__uint_as_float(us[2 * c2]) * sl2);
-          const float e1 = ex2(__uint_as_float(us[2 * c2 + 1]) * sl2);
-          pp[c2] = pack_bf16(e0, e1);
-          pd[c2] = pack_bf16(e0 * __uint_as_float(ud[2 * c2]), e1 * __uint_as_float(ud[2 * c2 + 1]));
-        }
       } else {
+        const bool full = __all_sync(0xffffffffu, cmin <= c0 && cmax >= c0 + 32);
 #pragma unroll
-        for (int c2 = 0; c2 < 32; ++c2) {
-          const int c = 2 * c2;
-          float e0 = ex2(__uint_as_float(us[c]) * sl2);
-          float e1 = ex2(__uint_as_float(us[c + 1]) * sl2);
-          e0 = (c >= cmin && c < cmax) ? e0 : 0.f;
-          e1 = (c + 1 >= cmin && c + 1 < cmax) ? e1 : 0.f;
-          const float d0 = (c >= cmin && c < cmax) ? e0 * __uint_as_float(ud[c]) : 0.f;
-          const float d1 = (c + 1 >= cmin && c + 1 < cmax) ? e1 * __uint_as_float(ud[c + 1]) : 0.f;
-          pp[c2] = pack_bf16(e0, e1);
-          pd[c2] = pack_bf16(d0, d1);
+        for (int c2 = 0; c2 < 16; ++c2) {
+          const float2 x = __fmul2_rn(make_float2(__uint_as_float(us[2 * c2]), __uint_as_float(us[2 * c2 + 1])), sl2);
+          float2 e;
+          if (c2 >= 16 - kPolyPairs) {
+            e = ex2_poly2(x);
+          } else {
+            e.x = ex2(x.x);
+            e.y = ex2(x.y);
+          }
+          if (!full) {
+            const int c = c0 + 2 * c2;
+            e.x = (c >= cmin && c < cmax) ? e.x : 0.f;
+            e.y = (c + 1 >= cmin && c + 1 < cmax) ? e.y : 0.f;
+          }
+          const float2 dd = __fmul2_rn(e, make_float2(__uint_as_float(ud[2 * c2]), __uint_as_float(ud[2 * c2 + 1])));
+          pp[c2] = pack_bf16(e.x, e.y);
+          pd[c2] = pack_bf16(dd.x, dd.y);
         }
       }
+      if (threadIdx.x == 0) TRACE(T_C_P, i);
       mbar_wait(&bar.pds_empty, (i & 1) ^ 1);
       tc_fence_after();
       // P^T and dS^T -> TMEM (A operands of the dV / dK TS-MMAs); dS^T also -> smem (B of dQ^T)
-      tmem_st32(tmem + lane_off + 128, pp);
-      tmem_st32(tmem + lane_off + 160, pd);
+      tmem_st16(tmem + lane_off + 128 + c0 / 2, pp);
+      tmem_st16(tmem + lane_off + 160 + c0 / 2, pd);
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        const uint32_t off = sw128_offset(r, ch);
+      for (int ch = 0; ch < 4; ++ch) {
+        const uint32_t off = sw128_offset(r, c0 / 8 + ch);
         *reinterpret_cast<uint4*>(sDS + off) = make_uint4(pd[4 * ch], pd[4 * ch + 1], pd[4 * ch + 2], pd[4 * ch + 3]);
       }
       tmem_wait_st();
       tc_fence_before();
       fence_async_smem();
       mbar_arrive(&bar.pds_full);
+      if (threadIdx.x == 0) TRACE(T_C_DS, i);
     }
-  } else {
+  } else if (warp < kWProd) {
     // ================= dQ drain WG: thread = head-dim lane d
-    const int d = (warp - 4) * 32 + lane;
-    const uint32_t lane_off = static_cast<uint32_t>((warp - 4) * 32) << 16;
+    const int d = (warp - kWDrain) * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>((warp - kWDrain) * 32) << 16;
     QIter it;
     it.begin(cu, p.tq, s0, s1, tok_first);
     for (int i = 0; it.valid(); it.next(), ++i) {
       mbar_wait(&bar.dq_full, i & 1);
       tc_fence_after();
+      if (threadIdx.x == kDrainT0) TRACE(T_D_DQ, i);
       uint32_t u[64];
       tmem_ld32(tmem + lane_off + 192, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
       tmem_ld32(tmem + lane_off + 192 + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bar.dq_empty);
-      // transpose through smem ([row][d] fp32) and reduce-add the tile into dq_acc with one
-      // TMA bulk tensor reduce
+      if (threadIdx.x == kDrainT0) TRACE(T_D_LD, i);
+      // transpose through smem ([row][d] fp32) and reduce-add into dq_acc with TMA bulk tensor
+      // reduces, one per 32-row half: reductions leave an SM at ~25 B/clk (profiles/
+      // r1_microbench.md), so the staging of one half overlaps the other half's egress
       if (p.ablate & 1) continue;
-      float* stg = reinterpret_cast<float*>(base + kOffStage);
-      if (threadIdx.x == 128) bulk_wait_read<0>();  // the previous tile's reduce has read the staging
-      named_bar_sync(1, 128);
+      const int row0 = cu[it.s] + it.tok;
 #pragma unroll
-      for (int c = 0; c < kBQ; ++c) stg[c * D + d] = __uint_as_float(u[c]);
-      fence_async_smem();
-      named_bar_sync(1, 128);
-      if (threadIdx.x == 128) {
-        tma_reduce_add_3d(mdq, stg, 0, hk * G, cu[it.s] + it.tok);
-        bulk_commit();
+      for (int hh = 0; hh < 2; ++hh) {
+        float* stg = reinterpret_cast<float*>(base + kOffStage + hh * (kStageBytes / 2));
+        if (threadIdx.x == kDrainT0) bulk_wait_read<1>();  // this half's previous reduce has read it
+        named_bar_sync(1, 128);
+#pragma unroll
+        for (int c = 0; c < kBQ / 2; ++c) stg[c * D + d] = __uint_as_float(u[hh * (kBQ / 2) + c]);
+        fence_async_smem();
+        named_bar_sync(1, 128);
+        if (threadIdx.x == kDrainT0) {
+          const int rr = hh * (kBQ / 2);  // first tile row of the half: token rr / G, head rr % G
+          tma_reduce_add_3d(mdq, stg, 0, hk * G + rr % G, row0 + rr / G);
+          bulk_commit();
+        }
       }
+      if (threadIdx.x == kDrainT0) TRACE(T_D_END, i);
     }
-    if (threadIdx.x == 128) bulk_wait<0>();
+    if (threadIdx.x == kDrainT0) bulk_wait<0>();
   }
 
   // ================= dK / dV epilogue: warps 0-3 dK, warps 4-7 dV (thread = key row)
@@ -484,13 +506,15 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kWProd) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
 }
 
 }  // namespace bwd
+
+DKV_TRACE_READ_FN(dkv_trace_read_v1)
 
 // DKV_BWD_V2=1: bwd2_sm100.cu's 128x128-tile kernel instead of the 64-row one below (experimental:
 // same speed today, and its dS uses the bf16-rounded P -- see DESIGN.md §4.2c)
@@ -519,12 +543,13 @@ int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, c
   Params p{};
   const int G = a.heads / a.kv_heads;
   const int tq = kBQ / G;
+  const int hb = G < kBQ / 2 ? G : kBQ / 2, tb = (kBQ / 2) / hb;  // dQ reduce box: one 32-row half
   if (a.total_q > 0 &&
       (!make_map_3d_bf16(&p.tm_q, a.q, a.total_q, a.heads, D, G, tq) ||
        !make_map_3d_bf16(&p.tm_do, a.dout, a.total_q, a.heads, D, G, tq) ||
        !make_map_3d_bf16(&p.tm_k, a.k, a.total_q, a.kv_heads, D, 1, kBK) ||
        !make_map_3d_bf16(&p.tm_v, a.v, a.total_q, a.kv_heads, D, 1, kBK) ||
-       !make_map_3d_f32(&p.tm_dq, w.dq_acc, a.total_q, a.heads, D, G, tq, D) ||
+       !make_map_3d_f32(&p.tm_dq, w.dq_acc, a.total_q, a.heads, D, hb, tb, D) ||
        !make_map_2d_bf16_sw32(&p.tm_x, w.xsplit, static_cast<int64_t>(w.tpad) * a.heads, 32, 16, kBQ))) {
     set_error("cuTensorMapEncodeTiled failed (backward q/dO/k/v/dq/x)");
     return DKV_ERR_CUDA;
@@ -540,7 +565,7 @@ int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, c
   if (with_self &&
       (!make_map_3d_bf16(&p.tm_qs, self->q, a.ctx_len, a.heads, D, G, tq) ||
        !make_map_3d_bf16(&p.tm_dos, self->dout, a.ctx_len, a.heads, D, G, tq) ||
-       !make_map_3d_f32(&p.tm_dqs, w.dq_acc_s, a.ctx_len, a.heads, D, G, tq, D) ||
+       !make_map_3d_f32(&p.tm_dqs, w.dq_acc_s, a.ctx_len, a.heads, D, hb, tb, D) ||
        !make_map_2d_bf16_sw32(&p.tm_xs, w.xsplit_s, static_cast<int64_t>(w.tpad_s) * a.heads, 32, 16, kBQ))) {
     set_error("cuTensorMapEncodeTiled failed (backward fused Call 1 maps)");
     return DKV_ERR_CUDA;
