@@ -32,6 +32,9 @@ DKV_DEVICE bool elect_one() {
 DKV_DEVICE void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+DKV_DEVICE void named_bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // per-warpgroup register budget (all 4 warps of an aligned warpgroup must execute it)
 template <int N>

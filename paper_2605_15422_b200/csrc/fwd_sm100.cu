@@ -20,10 +20,12 @@
 //   * TMEM: S_A [0,128) S_B [128,256) O_A [256,256+d) O_B [384,384+d) columns.
 //   * Online softmax in the log2 domain, one query row per thread (TMEM lane),
 //     with lazy O rescaling (only when the running max grows by > 8).
-//   * Roles: warps 0-3 softmax(A), 4-7 softmax(B), 8 TMA producer + TMEM
-//     allocator, 9 MMA issuer.
+//   * Roles: warps 0-7 softmax(A), 8-15 softmax(B) -- two warps per TMEM lane quadrant, one
+//     per 64-key half of each row --, 16 TMA producer + TMEM allocator, 17 MMA issuer
+//     (setmaxnreg: 112 registers for softmax warps, 56 for warpgroup 4).
 #include "dkv_internal.h"
 #include "tma_host.h"
+#include "trace.cuh"
 
 #include <cstdlib>
 
@@ -32,9 +34,20 @@ namespace fwd {
 
 constexpr int kBM = 128;  // rows per Q tile
 constexpr int kBN = 128;  // keys per KV tile
-constexpr int kThreads = 320;
+constexpr int kThreads = 640;  // 16 softmax warps, producer, MMA issuer, 2 idle (warpgroup 4)
+constexpr int kWProd = 16, kWMma = 17;
+constexpr int kRegsSoftmax = 112, kRegsOther = 56;  // setmaxnreg split (launch: 96 per thread)
+#ifndef FWD_SETMAXNREG
+#define FWD_SETMAXNREG 0  // 1 deadlocks (5 warps per sub-partition); the softmax fits 96 registers
+#endif
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-constexpr int kPolyPairs = 5;              // of every 16 exponential pairs, on the FMA pipe
+#ifndef FWD_ALTERNATE
+#define FWD_ALTERNATE 0  // strict A/B alternation measured slower (9.3 vs 8.6 ms at C3)
+#endif
+#ifndef FWD_POLY
+#define FWD_POLY 5
+#endif
+constexpr int kPolyPairs = FWD_POLY;       // of every 16 exponential pairs, on the FMA pipe
 
 template <int D>
 struct Cfg {
@@ -43,7 +56,7 @@ struct Cfg {
   static constexpr int kPanelBytes = kBM * 128;    // one 64-column SW128 panel of 128 rows
   static constexpr int kStages = D == 128 ? 2 : 3; // K ring and V ring depth
   static constexpr int kSmemTiles = (2 + 2 * kStages) * kTileBytes;
-  static constexpr int kSmemBytes = kSmemTiles + 1024 /*barriers*/ + 1024 /*align slack*/;
+  static constexpr int kSmemBytes = kSmemTiles + 8192 /*barriers + row-max exchange*/ + 1024 /*align slack*/;
 };
 
 struct Params {
@@ -63,7 +76,10 @@ struct Smem {
   uint64_t q_full;
   uint64_t k_full[4], k_empty[4], v_full[4], v_empty[4];
   uint64_t s_full[2], p_full[2], o_full[2];
+  uint64_t turn[2];  // FWD_ALTERNATE: turn[t] = the other tile's softmax finished this round
   uint32_t tmem_base;
+  // the two column halves of a row exchange partial row maxima (and, at the end, row sums)
+  float xch[2][2][2][128];  // [tile][iteration parity][column half][row]
 };
 
 template <int D>
@@ -135,12 +151,13 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.s_full[i], 1);
-      mbar_init(&sm.p_full[i], 128);
+      mbar_init(&sm.p_full[i], 256);
       mbar_init(&sm.o_full[i], 1);
+      mbar_init(&sm.turn[i], 256);
     }
     fence_mbar_init();
   }
-  if (warp == 8) tmem_alloc<512>(&sm.tmem_base);
+  if (warp == kWProd) tmem_alloc<512>(&sm.tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -156,8 +173,16 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     return n_ctx - 1 - (it - n_own);
   };
 
-  if (warp == 8) {
+  // teardown without a common tail (each role keeps its own register budget to the end): all
+  // warps arrive on barrier 15 when done with TMEM; the allocating warp waits there and frees it
+  auto done = [&]() {
+    tc_fence_before();
+    named_bar_arrive(15, kThreads);
+  };
+
+  if (warp == kWProd) {
     // ================= TMA producer
+    if (FWD_SETMAXNREG) regs_dec<kRegsOther>();
     if (elect_one()) {
       tma_prefetch(mq);
       tma_prefetch(mk_own);
@@ -182,6 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         const CUtensorMap* mv = is_ctx ? &p.tm_vc : mv_own;
         const int row = is_ctx ? j * kBN : seq0 + j * kBN;
         mbar_wait(&sm.k_empty[slot], ph ^ 1);
+        TRACE(T_Q_LOAD, it);
         mbar_arrive_expect_tx(&sm.k_full[slot], C::kTileBytes);
         for (int pn = 0; pn < C::kPanels; ++pn)
           tma_load_3d_hint(sK + slot * C::kTileBytes + pn * C::kPanelBytes, mk, &sm.k_full[slot], pn * 64, hk,
@@ -193,8 +219,14 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
                            row, pol_kv);
       }
     }
-  } else if (warp == 9) {
+    __syncwarp();
+    tc_fence_before();
+    named_bar_sync(15, kThreads);
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  } else if (warp == kWMma) {
     // ================= MMA issuer (one thread)
+    if (FWD_SETMAXNREG) regs_dec<kRegsOther>();
     if (elect_one()) {
       const uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, false, false);
       const uint32_t idesc_o = idesc_bf16_f32(kBM, D, false, true);
@@ -236,9 +268,11 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         for (int t = 0; t < ntile; ++t) {
           mbar_wait(&sm.p_full[t], it & 1);
           tc_fence_after();
+          TRACE(t == 0 ? T_ISS_DV : T_ISS_DK, it);
           issue_pv(t, vslot, it > 0);
           if (t == ntile - 1) mma_commit(&sm.v_empty[vslot]);
           if (more) {
+            TRACE(t == 0 ? T_ISS_S : T_ISS_DP, it + 1);
             issue_s(t, nslot);
             mma_commit(&sm.s_full[t]);
             if (t == ntile - 1) mma_commit(&sm.k_empty[nslot]);
@@ -248,11 +282,23 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         }
       }
     }
+    __syncwarp();
+    done();
+  } else if (warp > kWMma) {
+    if (FWD_SETMAXNREG) regs_dec<kRegsOther>();  // idle warps 18-19 complete warpgroup 4's register hand-back
+    done();
   } else {
-    // ================= softmax warpgroups: thread = one row of Q tile `t`
-    const int t = warp >> 2;
-    const int row = (warp & 3) * 32 + lane;
-    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    // ================= softmax: two warps per row quadrant and tile, thread = one row x 64
+    // keys (column half h).  One warp per sub-partition is latency-bound (tools/trace_fwd.py:
+    // ~2000 clk for a 128-key row), two interleave.  The halves exchange partial row maxima
+    // through shared memory (named barrier per warp pair) and take identical rescale decisions;
+    // each keeps a partial row sum, combined once in the epilogue.
+    const int t = warp >> 3;
+    const int h = (warp >> 2) & 1;
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int bar_id = 1 + t * 4 + q;  // the two warps (h = 0, 1) of this row quadrant
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t tS = tmem + lane_off + t * 128;
     const uint32_t tO = tmem + lane_off + 256 + t * 128;
     const bool tile_ok = (t == 0) || has_b;
@@ -260,6 +306,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     const int head = hk * p.group + row % p.group;
     const bool row_valid = tile_ok && qtok < rlen;
     const int qmin = tok0 + t * p.tq;                  // first token of the tile
+    const int cb = 64 * h;                             // first key column of this half
+    constexpr int kDH = D / 2;                         // O columns this half rescales / stores
+    if (FWD_SETMAXNREG) regs_inc<kRegsSoftmax>();
     float m_run = -INFINITY, l_run = 0.f;
     if (tile_ok) {
       for (int it = 0; it < n_iter; ++it) {
@@ -267,34 +316,51 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         const int j = tile_of(it, is_ctx);
         mbar_wait(&sm.s_full[t], it & 1);
         tc_fence_after();
-        float s[kBN];
+        if (threadIdx.x == 0) TRACE(T_C_S, it);
+        float s[64];
         {
-          uint32_t u[kBN];
-#pragma unroll
-          for (int c = 0; c < kBN / 32; ++c)
-            tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&u[c * 32]));
+          uint32_t u[64];
+          tmem_ld32(tS + cb, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
+          tmem_ld32(tS + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < kBN; ++i) s[i] = __uint_as_float(u[i]);
+          for (int i = 0; i < 64; ++i) s[i] = __uint_as_float(u[i]);
         }
+        if (threadIdx.x == 0) TRACE(T_C_DP, it);
+#if FWD_ALTERNATE
+        // strict A/B alternation of the two tiles' softmax: each then has the sub-partitions'
+        // MUFU pipes to itself (~half the time of two overlapping) and hides under the other
+        // tile's MMAs.  A waits for B's previous round, B for A's current one.
+        if (has_b) {
+          if (t == 0 && it > 0) mbar_wait(&sm.turn[0], (it - 1) & 1);
+          if (t == 1) mbar_wait(&sm.turn[1], it & 1);
+        }
+#endif
         // masks: own tiles on/after the tile's first token are causal; the last
         // context tile may be partial (keys >= P are out of bounds)
-        const int kbase = j * kBN;
-        const bool need_mask = is_ctx ? (kbase + kBN > p.ctx_len) : (kbase + kBN - 1 > qmin);
+        const int kbase = j * kBN + cb;
+        const bool need_mask = is_ctx ? (kbase + 64 > p.ctx_len) : (kbase + 63 > qmin);
         if (need_mask) {
           const int lim = is_ctx ? p.ctx_len - 1 - kbase : qtok - kbase;  // last visible column
 #pragma unroll
-          for (int c = 0; c < kBN; ++c)
+          for (int c = 0; c < 64; ++c)
             if (c > lim) s[c] = -INFINITY;
         }
-        // row max: 4 independent chains of 3-input max (FMNMX3) + a short tree (one 128-long
-        // dependent chain would sit on the softmax critical path)
-        float m4[4] = {s[0], s[1], s[2], s[3]};
+        // partial row max (8 independent FMNMX3 chains), then the other half's through smem
+        float m8[8];
 #pragma unroll
-        for (int c = 4; c < kBN; c += 8)
+        for (int i = 0; i < 8; ++i) m8[i] = fmax3(s[i], s[8 + i], s[16 + i]);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) m4[i] = fmax3(m4[i], s[c + 2 * i], s[c + 2 * i + 1]);
-        const float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
+        for (int c = 24; c < 56; c += 16)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) m8[i] = fmax3(m8[i], s[c + i], s[c + 8 + i]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m8[i] = fmaxf(m8[i], s[56 + i]);
+        float mx = fmaxf(fmax3(m8[0], m8[1], m8[2]), fmax3(fmax3(m8[3], m8[4], m8[5]), m8[6], m8[7]));
+        sm.xch[t][it & 1][h][row] = mx;
+        named_bar_sync(bar_id, 64);  // also: both halves' S loads are done before P overwrites S
+        mx = fmaxf(mx, sm.xch[t][it & 1][h ^ 1][row]);
+        if (threadIdx.x == 0) TRACE(T_ISS_DQ, it);
         const float m_tile = mx * p.scale_log2;
         const float m_new = fmaxf(m_run, m_tile);
         float alpha = 1.f;
@@ -307,9 +373,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         // 16 pairs on the FMA pipe (polynomial, f32x2) to unload the MUFU pipe; row sum in FADD2
         const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
         const float2 nm2 = make_float2(-m_use, -m_use);
-        float2 rs2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        float2 rs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int c0 = 0; c0 < kBN; c0 += 32) {
+        for (int c0 = 0; c0 < 64; c0 += 32) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -321,18 +387,18 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
               e.x = ex2(x.x);
               e.y = ex2(x.y);
             }
-            rs2[i & 1] = __fadd2_rn(rs2[i & 1], e);
+            rs2[i & 3] = __fadd2_rn(rs2[i & 3], e);
             pk[i] = pack_bf16(e.x, e.y);
           }
-          tmem_st16(tS + c0 / 2, pk);
+          tmem_st16(tS + (cb + c0) / 2, pk);  // P (bf16 pairs) over the S columns
         }
-        const float2 rsum = __fadd2_rn(rs2[0], rs2[1]);
-        const float rowsum = rsum.x + rsum.y;
-        l_run = l_run * alpha + rowsum;
-        // O holds P V of iterations < it (its MMA completed before S(it) did)
+        const float2 rsum = __fadd2_rn(__fadd2_rn(rs2[0], rs2[1]), __fadd2_rn(rs2[2], rs2[3]));
+        l_run = l_run * alpha + (rsum.x + rsum.y);
+        // O holds P V of iterations < it (its MMA completed before S(it) did); each half
+        // rescales its D/2 columns
         if (it > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-          for (int c0 = 0; c0 < D; c0 += 32) {
+          for (int c0 = h * kDH; c0 < (h + 1) * kDH; c0 += 32) {
             uint32_t r[32];
             tmem_ld32(tO + c0, r);
             tmem_wait_ld();
@@ -346,17 +412,25 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
             tmem_st32(tO + c0, r);
           }
         }
+        if (threadIdx.x == 0) TRACE(T_MMA_END, it);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&sm.p_full[t]);
+        if (threadIdx.x == 0) TRACE(T_C_P, it);
+#if FWD_ALTERNATE
+        if (has_b) mbar_arrive(&sm.turn[t ^ 1]);
+#endif
       }
-      // ---- epilogue: O / l -> bf16, lse
+      // ---- epilogue: l = both halves' partial sums; O / l -> bf16 (each half D/2 columns), lse
+      sm.xch[t][n_iter & 1][h][row] = l_run;
+      named_bar_sync(bar_id, 64);
+      l_run += sm.xch[t][n_iter & 1][h ^ 1][row];
       mbar_wait(&sm.o_full[t], 0);
       tc_fence_after();
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
       __nv_bfloat16* orow = out + (static_cast<int64_t>(seq0 + qtok) * p.heads + head) * D;
 #pragma unroll 1
-      for (int c0 = 0; c0 < D; c0 += 32) {
+      for (int c0 = h * kDH; c0 < (h + 1) * kDH; c0 += 32) {
         uint32_t r[32];
         tmem_ld32(tO + c0, r);
         tmem_wait_ld();
@@ -371,16 +445,11 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
           for (int i = 0; i < 4; ++i) dst[i] = v[i];
         }
       }
-      if (row_valid)
+      if (row_valid && h == 0)
         lse_out[static_cast<int64_t>(head) * lse_stride + seq0 + qtok] =
             (m_run + __log2f(l_run)) * 0.6931471805599453f;
     }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 8) {
-    tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    done();
   }
 }
 
@@ -443,6 +512,8 @@ int launch(const SimtArgs& a, const CtxSelf* self, cudaStream_t st) {
 }
 
 }  // namespace fwd
+
+DKV_TRACE_READ_FN(dkv_trace_read_fwd)
 
 bool force_simt() {
   static const bool f = [] {

@@ -15,7 +15,8 @@ from oracle import dualkv_oracle as orc
 
 pytestmark = pytest.mark.gpu
 
-# (seed, N, P, R list, H, Hk, d): ragged, partial tiles, R_i = 0, P = 0, G in {1,2,4,8}
+# (seed, N, P, R list, H, Hk, d): ragged, partial tiles, R_i = 0, P = 0, G in {1,2,4,8,16,32,64}
+# (G >= 32: a backward query tile holds <= 2 tokens and the dQ reduce box splits heads)
 BF16_CASES = [
     (1, 3, 300, [77, 0, 260], 8, 2, 128),
     (2, 2, 128, [128, 129], 4, 1, 128),
@@ -25,6 +26,9 @@ BF16_CASES = [
     (6, 3, 257, [64, 65, 190], 16, 2, 64),
     (7, 5, 100, [20, 0, 0, 41, 140], 32, 8, 128),
     (8, 2, 513, [256, 3], 4, 4, 128),
+    (9, 2, 130, [70, 5], 16, 1, 128),
+    (10, 3, 64, [3, 1, 9], 32, 1, 128),
+    (11, 2, 129, [2, 4], 64, 1, 128),
 ]
 
 
