@@ -12,6 +12,8 @@
 
 #include "dkv_internal.h"
 
+#include <cstdlib>
+
 namespace dkv {
 
 static thread_local std::string g_err;
@@ -126,6 +128,13 @@ static int fwd_impl(const dkv_fwd_params* p, bool dualkv, void* stream, const ch
 // context work chunk (sequences per context work unit) for the tensor-core backward
 static int auto_chunk(const dkv_bwd_params* p) {
   if (p->ctx_chunk > 0) return static_cast<int>(std::min<int64_t>(p->ctx_chunk, p->num_seqs));
+  {
+    static const int env_chunk = [] {  // DKV_CTX_CHUNK: tuning experiments only
+      const char* e = getenv("DKV_CTX_CHUNK");
+      return e ? atoi(e) : 0;
+    }();
+    if (env_chunk > 0) return static_cast<int>(std::min<int64_t>(env_chunk, p->num_seqs));
+  }
   if (p->ctx_len == 0) return static_cast<int>(p->num_seqs);
   const bool tc = tc_bwd_supported(p->dtype, static_cast<int>(p->head_dim), static_cast<int>(p->heads),
                                    static_cast<int>(p->kv_heads));
