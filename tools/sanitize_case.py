@@ -1,0 +1,18 @@
+"""Small two-call DualKV fwd+bwd (ragged, partial tiles, R_i = 0, G = 4) for compute-sanitizer."""
+import os, sys
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2605_15422_b200 as dkv  # noqa: E402
+g = torch.Generator(device="cuda").manual_seed(0)
+mk = lambda *s: torch.randn(*s, device="cuda", generator=g).to(torch.bfloat16)
+p, rl, h, hk, d = 200, [77, 0, 150, 33], 8, 2, 128
+t = sum(rl)
+qc, kc, vc, doc = mk(p, h, d), mk(p, hk, d), mk(p, hk, d), mk(p, h, d)
+q, kd, vd, dod = mk(t, h, d), mk(t, hk, d), mk(t, hk, d), mk(t, h, d)
+dec = dkv.DualKVInput(q, kc, vc, kd, vd, np.concatenate([[0], np.cumsum(rl)]))
+oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc, dec)
+for det in (True, False):
+    gr = dkv.dualkv_two_call_bwd(qc, dec, oc, lc, doc, od, ld, dod, deterministic=det)
+torch.cuda.synchronize()
+print("ok", [float(x.float().abs().sum()) for x in gr])
