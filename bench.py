@@ -348,6 +348,29 @@ def main():
                "pair_ratio": round(visible_pairs(p, rl0, "standard") / pairs0, 3)}
         del qr, kr, vr, dor, rb
 
+    # ---- the step before attention: repack N(P+R) -> P+NR fused with RoPE at
+    # logical positions, HBM-bound -- reported against the measured copy bandwidth
+    repack = None
+    if not args.no_replicated and dt == torch.bfloat16:
+        from paper_2605_15422_b200 import packing as pk
+        plan = pk.make_plan([(p, rl0)])
+        xs = [mk(plan.total_standard, hh, d) for hh in (h, hk, hk)]
+        dkv.repack_rope_to_dualkv(*xs, plan, 1e6)
+        rp_ms = timed(lambda: dkv.repack_rope_to_dualkv(*xs, plan, 1e6), args.steps)
+        moved = 2 * plan.total_dualkv * (h + 2 * hk) * d * 2  # gathered rows read + written once
+        hbm = peaks_hbm = None
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                peaks_hbm = json.load(f).get("hbm_gbs")
+        except Exception:
+            pass
+        gbs = moved / (rp_ms * 1e-3) / 1e9
+        repack = {"ms": round(rp_ms, 4), "bytes": moved, "GB_per_s": round(gbs, 1),
+                  "frac_of_hbm": round(gbs / peaks_hbm, 3) if peaks_hbm else None,
+                  "what": "repack_rope_to_dualkv: q,k,v gathered from the replicated layout, q,k rotated at "
+                          "logical positions (prompt j -> j, response r -> P + r), one group"}
+        del xs
+
     e2e = None
     if not args.no_e2e:
         t0 = sum(rl0)
@@ -503,7 +526,7 @@ def main():
             "bwd_tflops": round(10 * pairs0 * h * d / (bwd_ms * 1e-3) / 1e12, 2),
             "separate_calls_ms_group0": round(sep_ms, 3),
             "step_frac_of_peak": step_frac,
-            "replicated_ncopy": rep, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "replicated_ncopy": rep, "repack_rope": repack, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
             "gpu_launches": int(al.value), "clocks": clk,
         }
         print(json.dumps(line), flush=True)

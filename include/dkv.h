@@ -148,6 +148,22 @@ DKV_API int32_t dkv_segment_sum_rows(const void* src, void* dst, int32_t dtype, 
                              const int64_t* seg, const int64_t* src_idx, int64_t n_rows,
                              void* stream);
 
+/* RoPE at logical positions (reference layer.py:182-205, positions packing.py:105-120), fused
+ * with an optional row gather (the N(P+R) -> P+NR repack, packing.py:182-220):
+ *   dst[r, h, 2k:2k+2] = R(pos[r] * base^(-2k/d)) src[idx ? idx[r] : r, h, 2k:2k+2]
+ * (R the 2x2 rotation, transposed when `inverse` -- the adjoint, rope_bwd).  Angles in fp64,
+ * rotation in fp32, dtype storage (bf16 or fp32) for src and dst; `positions` and `idx` are
+ * device int64 arrays of n_rows.  head_dim a multiple of 8 (bf16) / 4 (fp32), 16-byte aligned rows. */
+DKV_API int32_t dkv_rope_rows(const void* src, void* dst, int32_t dtype, int64_t n_rows, int64_t heads,
+                              int64_t head_dim, const int64_t* positions, const int64_t* idx, double base,
+                              int32_t inverse, void* stream);
+/* The same for a row's q [heads], k [kv_heads] (rotated) and v [kv_heads] (copied) in one pass --
+ * the fused repack + RoPE of the QKV projections; any tensor's src/dst may both be NULL. */
+DKV_API int32_t dkv_rope_qkv_rows(const void* q_src, const void* k_src, const void* v_src, void* q_dst,
+                                  void* k_dst, void* v_dst, int32_t dtype, int64_t n_rows, int64_t heads,
+                                  int64_t kv_heads, int64_t head_dim, const int64_t* positions,
+                                  const int64_t* idx, double base, int32_t inverse, void* stream);
+
 /* Kernel timing for the bench harness: while enabled, the library records a
  * CUDA event pair (on the launching stream) around every main attention
  * kernel and counts every kernel it launches.  dkv_profile_end synchronises

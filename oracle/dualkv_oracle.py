@@ -443,6 +443,23 @@ def position_ids(groups, mode="dualkv"):
     return np.asarray(pos, dtype=np.int64)
 
 
+def rope(x, positions, base=10000.0, inverse=False):
+    """Rotary embedding at (logical) positions, f64 (layer.py:182-196; inverse = rope_bwd,
+    layer.py:198-205): pair (2k, 2k+1) rotated by pos * base^(-2k/d)."""
+    x = np.asarray(x, dtype=np.float64)
+    d = x.shape[-1]
+    inv_freq = base ** (-np.arange(0, d, 2, dtype=np.float64) / d)
+    ang = np.asarray(positions, dtype=np.float64)[:, None] * inv_freq[None, :]
+    cos, sin = np.cos(ang)[:, None, :], np.sin(ang)[:, None, :]
+    if inverse:
+        sin = -sin
+    ev, od = x[..., 0::2], x[..., 1::2]
+    out = np.empty_like(x)
+    out[..., 0::2] = ev * cos - od * sin
+    out[..., 1::2] = ev * sin + od * cos
+    return out
+
+
 def repack_index(groups):
     """For every row of the shared layout, the source row in the replicated
     layout (prompt rows taken from copy 0).  Gathering a replicated

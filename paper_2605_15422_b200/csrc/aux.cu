@@ -4,7 +4,10 @@
 //     (kernel.py:279-285 / convert_dkv_context kernel.py:140-148)
 //   * f32 -> storage cast (dQ accumulator, generic convert)
 //   * row gather / segment-sum for the N(P+R) <-> P+NR repack (packing.py:159-220)
+//   * RoPE at logical positions, optionally fused with the repack gather (layer.py:182-205)
 #include "dkv_internal.h"
+
+#include <algorithm>
 
 namespace dkv {
 
@@ -263,6 +266,140 @@ extern "C" int32_t dkv_segment_sum_rows(const void* src, void* dst, int32_t dtyp
     return DKV_ERR_CUDA;
   }
   return DKV_OK;
+}
+
+// RoPE: one CTA per destination row, for up to three tensors of that row (q and k rotated, v
+// copied -- the fused repack + RoPE of the QKV projections).  The row's d/2 angles
+// pos * base^(-2k/d) are formed in fp64 (|angle| reaches ~2e4 rad at long prompts), reduced
+// mod 2 pi in fp64 and only then taken through fp32 sincos; the (cos, sin) pairs are shared by
+// every head of q and k.  Pairs move as 16-byte vectors (4 bf16 / 2 fp32 pairs): HBM-bound.
+template <typename T>
+DKV_DEVICE void rope_vec(uint4& v, const float* cs, int half, int k0) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+  if constexpr (sizeof(T) == 2) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float c = cs[k0 + j], sn = cs[half + k0 + j];
+      const float ev = __uint_as_float(w[j] << 16), od = __uint_as_float(w[j] & 0xffff0000u);
+      __nv_bfloat162 o = __floats2bfloat162_rn(ev * c - od * sn, ev * sn + od * c);
+      w[j] = *reinterpret_cast<uint32_t*>(&o);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float c = cs[k0 + j], sn = cs[half + k0 + j];
+      const float ev = __uint_as_float(w[2 * j]), od = __uint_as_float(w[2 * j + 1]);
+      w[2 * j] = __float_as_uint(ev * c - od * sn);
+      w[2 * j + 1] = __float_as_uint(ev * sn + od * c);
+    }
+  }
+}
+
+struct RopeArgs {
+  const void* src[3];
+  void* dst[3];
+  int64_t heads[3];  // 0: tensor absent
+  int rotate[3];
+  int64_t head_dim;
+  const int64_t* positions;
+  const int64_t* idx;
+  double base;
+  int inverse;
+};
+
+template <typename T>
+__global__ void rope_rows_kernel(const RopeArgs a) {
+  extern __shared__ float cs[];  // [d/2] cos, [d/2] sin
+  const int64_t r = blockIdx.x;
+  const int half = static_cast<int>(a.head_dim / 2);
+  const double pos = static_cast<double>(a.positions[r]);
+  for (int k = threadIdx.x; k < half; k += blockDim.x) {
+    const double inv_freq = exp2(-2.0 * k / static_cast<double>(a.head_dim) * log2(a.base));
+    double ang = pos * inv_freq;
+    ang -= 6.283185307179586 * rint(ang * 0.15915494309189535);  // to [-pi, pi]
+    float sf, cf;
+    sincosf(static_cast<float>(ang), &sf, &cf);
+    cs[k] = cf;
+    cs[half + k] = a.inverse ? -sf : sf;
+  }
+  __syncthreads();
+  const int64_t sr = a.idx ? a.idx[r] : r;
+  constexpr int kPairs = sizeof(T) == 2 ? 4 : 2;  // pairs per 16-byte vector
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    if (a.heads[t] == 0) continue;
+    const int64_t nvec = a.heads[t] * half / kPairs;
+    const uint4* in = reinterpret_cast<const uint4*>(static_cast<const T*>(a.src[t]) + sr * a.heads[t] * a.head_dim);
+    uint4* out = reinterpret_cast<uint4*>(static_cast<T*>(a.dst[t]) + r * a.heads[t] * a.head_dim);
+    for (int64_t i = threadIdx.x; i < nvec; i += blockDim.x) {
+      uint4 v = in[i];
+      if (a.rotate[t]) rope_vec<T>(v, cs, half, static_cast<int>((i * kPairs) % half));
+      out[i] = v;
+    }
+  }}
+
+extern "C" int32_t dkv_rope_qkv_rows(const void* q_src, const void* k_src, const void* v_src, void* q_dst,
+                                     void* k_dst, void* v_dst, int32_t dtype, int64_t n_rows, int64_t heads,
+                                     int64_t kv_heads, int64_t head_dim, const int64_t* positions,
+                                     const int64_t* idx, double base, int32_t inverse, void* stream) {
+  const int pairs_per_vec = dtype == DKV_BF16 ? 4 : 2;
+  if (n_rows < 0 || heads < 0 || kv_heads < 0 || head_dim <= 0 || !(base > 0.0) ||
+      (dtype != DKV_BF16 && dtype != DKV_F32) || (n_rows > 0 && !positions)) {
+    set_error("dkv_rope_qkv_rows: invalid arguments");
+    return DKV_ERR_INVALID;
+  }
+  RopeArgs a{};
+  const void* srcs[3] = {q_src, k_src, v_src};
+  void* dsts[3] = {q_dst, k_dst, v_dst};
+  const int64_t hs[3] = {heads, kv_heads, kv_heads};
+  int64_t maxvec = 0;
+  for (int t = 0; t < 3; ++t) {
+    if (!srcs[t] && !dsts[t]) continue;
+    if (!srcs[t] || !dsts[t] || hs[t] <= 0 || (srcs[t] == dsts[t] && idx) ||
+        (reinterpret_cast<uintptr_t>(srcs[t]) & 15) || (reinterpret_cast<uintptr_t>(dsts[t]) & 15)) {
+      set_error("dkv_rope_qkv_rows: tensor pointers must be 16-byte aligned pairs (no in-place gather)");
+      return DKV_ERR_INVALID;
+    }
+    a.src[t] = srcs[t];
+    a.dst[t] = dsts[t];
+    a.heads[t] = hs[t];
+    a.rotate[t] = t < 2;
+    maxvec = std::max<int64_t>(maxvec, hs[t] * head_dim / 2 / pairs_per_vec);
+  }
+  if ((head_dim / 2) % pairs_per_vec) {
+    set_error("dkv_rope_qkv_rows: head_dim must be a multiple of 8 (bf16) / 4 (fp32)");
+    return DKV_ERR_UNSUPPORTED;
+  }
+  if (n_rows == 0 || maxvec == 0) return DKV_OK;
+  a.head_dim = head_dim;
+  a.positions = positions;
+  a.idx = idx;
+  a.base = base;
+  a.inverse = inverse;
+  auto st = static_cast<cudaStream_t>(stream);
+  const size_t sm = static_cast<size_t>(head_dim) * sizeof(float);
+  const int threads = maxvec >= 256 ? 256 : (maxvec >= 128 ? 128 : 64);
+  if (dtype == DKV_BF16)
+    rope_rows_kernel<__nv_bfloat16><<<static_cast<unsigned>(n_rows), threads, sm, st>>>(a);
+  else
+    rope_rows_kernel<float><<<static_cast<unsigned>(n_rows), threads, sm, st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("dkv_rope_qkv_rows: ") + cudaGetErrorString(e));
+    return DKV_ERR_CUDA;
+  }
+  return DKV_OK;
+}
+
+extern "C" int32_t dkv_rope_rows(const void* src, void* dst, int32_t dtype, int64_t n_rows, int64_t heads,
+                                 int64_t head_dim, const int64_t* positions, const int64_t* idx, double base,
+                                 int32_t inverse, void* stream) {
+  if (n_rows > 0 && (!src || !dst)) {
+    set_error("dkv_rope_rows: invalid arguments");
+    return DKV_ERR_INVALID;
+  }
+  return dkv_rope_qkv_rows(src, nullptr, nullptr, dst, nullptr, nullptr, dtype, n_rows, heads, 0, head_dim,
+                           positions, idx, base, inverse, stream);
 }
 
 extern "C" int32_t dkv_convert_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream) {

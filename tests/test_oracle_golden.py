@@ -129,3 +129,18 @@ def test_stagnation_foil():
     for p in parts:
         acc += p
     assert float(orc.quantize(acc, "bf16")[0]) == 1.5
+
+
+def test_rope_vs_reference_golden():
+    """Oracle RoPE at DualKV logical positions == the reference's rope / rope_bwd
+    (layer.py:182-205), pinned by tests/golden/rope.npz (tools/make_golden_rope.py)."""
+    meta, rec = load_golden("rope")
+    for i, c in enumerate(meta["cases"]):
+        y = orc.rope(rec[f"x{i}"], rec["pos"], c["base"])
+        b = orc.rope(rec[f"x{i}"], rec["pos"], c["base"], inverse=True)
+        np.testing.assert_allclose(y, rec[f"y{i}"], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(b, rec[f"b{i}"], rtol=0, atol=1e-12)
+    yb = orc.rope(rec["x_big"], rec["pos_big"], meta["big_base"])
+    np.testing.assert_allclose(yb, rec["y_big"], rtol=0, atol=1e-12)
+    # the golden positions are the DualKV layout's (prompt j -> j, response r -> P + r)
+    np.testing.assert_array_equal(rec["pos"], orc.position_ids([(9, [4, 0, 6]), (3, [5])]))
