@@ -24,5 +24,6 @@ from .api import (  # noqa: F401
 )
 from .costmodel import attention_flops, visible_pairs  # noqa: F401
 from .rope import RoPE, repack_rope_to_dualkv, rope_logical  # noqa: F401
+from .layer import DualKVSelfAttention  # noqa: F401
 
 __version__ = "0.1.0"
