@@ -151,50 +151,67 @@ def run_reference(args):
 
 # ---------------------------------------------------------------- GPU side
 class ClockSampler:
-    def __init__(self, out_path=None):
-        self.samples = []
-        self.proc = None
-        self.out_path = out_path
+    """SM clocks and clock-event reasons polled through NVML every ~5 ms while running
+    (nvidia-smi's 100 ms loop would see one or two samples of a ~0.2 s timed region); falls
+    back to nvidia-smi when NVML is unavailable.  `start`/`stop` bracket the timed regions."""
+
+    REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown")]
+
+    def __init__(self):
+        self.samples = []   # (sm_mhz, reasons bitmask, gpu busy)
+        self.sm_max = None
+        self.nvml = None
+        self.running = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            idx = int(os.environ.get("LOCAL_RANK", "0"))
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                idx = int(vis.split(",")[idx])
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.sm_max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _poll(self):
+        n = self.nvml
+        while self.running:
+            try:
+                mhz = n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM)
+                rs = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((mhz, rs, not (rs & n.nvmlClocksEventReasonGpuIdle)))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def start(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        dev = os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0] or "0"
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(int(os.environ.get("LOCAL_RANK", "0"))) if dev.isdigit() else dev,
-                 f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except Exception:
-            self.proc = None
+        if self.nvml is None:
+            return
+        self.running = True
+        self.thread = threading.Thread(target=self._poll, daemon=True)
+        self.thread.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.samples.append([x.strip() for x in line.split(",")])
+    def pause(self):
+        if self.nvml is not None and self.running:
+            self.running = False
+            self.thread.join()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for s in self.samples:
-            for i, n in enumerate(names):
-                if len(s) > 4 + i and s[4 + i].lower().startswith("active"):
-                    reasons.add(n)
-        busy = [x for x in sm if x > 0]
-        return {"sm_mhz": float(np.median(busy)) if busy else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.samples)}
+        self.pause()
+        if self.nvml is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        busy = [m for m, _, b in self.samples if b] or [m for m, _, _ in self.samples]
+        reasons = sorted({name for name, attr in self.REASONS for _, rs, _ in self.samples
+                          if rs & getattr(self.nvml, attr, 0)})
+        return {"sm_mhz": float(np.median(busy)) if busy else None, "sm_max_mhz": self.sm_max,
+                "reasons": reasons, "samples": len(self.samples),
+                "window": "NVML polled every ~5 ms during the timed regions (main steps, fwd/bwd split)"}
 
 
 def main():
@@ -287,10 +304,10 @@ def main():
         return ms_
 
     clocks = ClockSampler()
-    clocks.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    clocks.start()
     # ---- headline: device-resident inputs, K steps, per-kernel CUDA events recorded by libdkv
     lib.dkv_profile_begin()
     ms = timed(step, args.steps)
@@ -316,6 +333,7 @@ def main():
                                 deterministic=False)
 
     bwd_ms = timed(bwd_only, args.steps)
+    clocks.pause()
     ctx_b = dkv.VarlenBatch(qc, kc, vc, np.array([0, p]))
 
     def step_separate():
