@@ -84,6 +84,22 @@ def test_c2_dualkv_equals_replicated(cuda_device):
     _check_equivalence(dkv, qc, kc, vc, q, kd, vd, doc, dod, np.arange(0, t + 1, r))
 
 
+@pytest.mark.parametrize("cfg", [(32, 8192, 2048, 32, 8), (32, 16384, 2048, 32, 4)], ids=["C3", "C5"])
+def test_headline_shapes_dualkv_equals_replicated(cfg, cuda_device):
+    """BASELINE configs C3 (the bench workload) and C5 (Qwen3-30B-A3B heads, G = 8, P = 16K) at
+    full size: the fused two-call DualKV op against replicated N-copy attention on the same
+    device (SURVEY §8c oracle 3), all outputs and six gradients."""
+    import paper_2605_15422_b200 as dkv
+    n, p, r, h, hk = cfg
+    d = 128
+    g = torch.Generator(device="cuda").manual_seed(11)
+    t = n * r
+    qc, kc, vc, doc = _rand(g, p, h, d), _rand(g, p, hk, d), _rand(g, p, hk, d), _rand(g, p, h, d)
+    q, kd, vd, dod = _rand(g, t, h, d), _rand(g, t, hk, d), _rand(g, t, hk, d), _rand(g, t, h, d)
+    _check_equivalence(dkv, qc, kc, vc, q, kd, vd, doc, dod, np.arange(0, t + 1, r))
+    torch.cuda.empty_cache()
+
+
 def test_ragged_group_through_device_repack(cuda_device):
     """C4-like ragged group (R_i ~ U[128, 1024]) packed N(P+R) -> P+NR on the device."""
     import paper_2605_15422_b200 as dkv
