@@ -47,7 +47,10 @@ constexpr int D = 128;
 constexpr int kThreads = 448;  // 8 compute warps, 4 dQ-drain warps, producer, MMA issuer
 constexpr int kWDrain = 8, kWProd = 12, kWMma = 13;
 constexpr int kDrainT0 = kWDrain * 32;  // first drain thread
-constexpr int kPolyPairs = 4;           // of every 16 exponential pairs, on the FMA pipe
+#ifndef BWD_POLY
+#define BWD_POLY 0  // sweep 0/2/4/6: 27.5/27.7/28.1/27.9 ms (noise-level; MUFU is not the limit here)
+#endif
+constexpr int kPolyPairs = BWD_POLY;    // of every 16 exponential pairs, on the FMA pipe
 constexpr int kStages = 3;
 constexpr int kKVBytes = kBK * D * 2;       // 32 KB
 constexpr int kKVPanel = kBK * 128;         // 16 KB
