@@ -326,12 +326,14 @@ def main():
     def fwd_only():
         saved["oc"], saved["lc"], saved["od"], saved["ld"] = dkv.dualkv_two_call_fwd(qc, dec0)
 
+    fwd_only()  # warm the allocator for this call pattern before timing it
     fwd_ms = timed(fwd_only, args.steps)
 
     def bwd_only():
         dkv.dualkv_two_call_bwd(qc, dec0, saved["oc"], saved["lc"], doc, saved["od"], saved["ld"], dod0,
                                 deterministic=False)
 
+    bwd_only()
     bwd_ms = timed(bwd_only, args.steps)
     clocks.pause()
     ctx_b = dkv.VarlenBatch(qc, kc, vc, np.array([0, p]))
@@ -343,6 +345,7 @@ def main():
         dkv.dualkv_bwd(dec0, od, ld, dod0, deterministic=False)
         dkv.fa2_varlen_bwd(ctx_b, oc, lc, doc)
 
+    step_separate()
     sep_ms = timed(step_separate, args.steps)
 
     rep = None
@@ -358,8 +361,29 @@ def main():
 
         rep_step()
         rep_ms = timed(rep_step, max(1, min(args.steps, 3)))
-        grp_ms = fwd_ms + bwd_ms
-        rep = {"ms_per_group": round(rep_ms, 3),
+        grp_ms = ms / max(1, len(my_r))  # the headline step (fwd+bwd of Call 1 + Call 2) per group
+        # the same replicated problem through a library kernel, for scale: FlashAttention-2
+        # (flash_attn 2.8.3, mma.sync SASS for sm_100) varlen causal fwd+bwd
+        ext = None
+        try:
+            from flash_attn import flash_attn_varlen_func
+            cu_t = torch.as_tensor(s_cu, dtype=torch.int32, device=dev)
+            mx = int(np.diff(s_cu).max())
+            qx, kx, vx = (x.detach().clone().requires_grad_() for x in (qr, kr, vr))
+
+            def fa2_step():
+                o = flash_attn_varlen_func(qx, kx, vx, cu_t, cu_t, mx, mx, causal=True)
+                o.backward(dor)
+
+            fa2_step()
+            fa2_ms = timed(fa2_step, max(1, min(args.steps, 3)))
+            ext = {"impl": "flash_attn 2.8.3 flash_attn_varlen_func (FA2, sm_100 build)",
+                   "ms_per_group": round(fa2_ms, 3),
+                   "speedup_dualkv_vs_fa2_ncopy": round(fa2_ms / (ms / max(1, len(my_r))), 3)}
+            del qx, kx, vx
+        except Exception as exc:  # library missing / unsupported on this build
+            ext = {"unavailable": str(exc)[:120]}
+        rep = {"ms_per_group": round(rep_ms, 3), "library_baseline": ext,
                "tflops_algorithmic": round(14 * visible_pairs(p, rl0, "standard") * h * d / (rep_ms * 1e-3) / 1e12, 2),
                "dualkv_ms_per_group": round(grp_ms, 3),
                "speedup_dualkv_vs_ncopy": round(rep_ms / grp_ms, 3),
