@@ -270,6 +270,10 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         const int xrow = (hk * xtpad + row0) * G;
         tma_load_2d(base + kOffX + st * 2 * kXBytes, mx, &bar.q_full[st], 0, xrow);
         tma_load_2d(base + kOffX + st * 2 * kXBytes + kXBytes, mx, &bar.q_full[st], 16, xrow);
+#ifdef DKV_TRACE
+        mbar_wait(&bar.q_full[st], (i / kStages) & 1);  // trace build: record the load's arrival
+        TRACE(T_DO_LOAD, i);
+#endif
       }
     }
   } else if (warp == kWMma) {

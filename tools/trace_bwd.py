@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2605_15422_b200 as dkv  # noqa: E402
 from paper_2605_15422_b200._lib import lib  # noqa: E402
 
-EV = ["Qld", "dOld", "iS", "idP", "idV", "idK", "idQ", "cS", "cP", "cdP", "cdS", "dDQ", "dLD", "dEND", "mEND"]
+EV = ["Qld", "Qarr", "iS", "idP", "idV", "idK", "idQ", "cS", "cP", "cdP", "cdS", "dDQ", "dLD", "dEND", "mEND"]
 cta = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 show = int(sys.argv[2]) if len(sys.argv) > 2 else 12
 n, p, r, h, hk, d = 32, 8192, 2048, 32, 8, 128
@@ -53,7 +53,7 @@ if valid:
                   ("compute dP -> dS done", 9, 10), ("dQ issue -> drain sees dQ", 6, 11), ("drain dQ -> loaded", 11, 12),
                   ("drain loaded -> chunks issued", 12, 13), ("dQ issue -> next dP issue", 6, 3)]
     else:
-        pairs_ = [("S issue -> compute sees S+dP", 2, 7), ("compute TMEM loads", 7, 9), ("compute math", 9, 8), ("compute waits pds_empty+stores", 8, 10),
+        pairs_ = [("Q/dO load issue -> arrival", 0, 1), ("S issue -> compute sees S+dP", 2, 7), ("compute TMEM loads", 7, 9), ("compute math", 9, 8), ("compute waits pds_empty+stores", 8, 10),
                   ("pds_full -> dV issue", 10, 4), ("dV issue -> dQ issue", 4, 6), ("dQ issue -> drain sees dQ", 6, 11),
                   ("drain dQ -> loaded", 11, 12), ("drain loaded -> halves issued", 12, 13)]
     for nm, a, b in pairs_:
