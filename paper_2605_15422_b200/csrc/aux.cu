@@ -8,6 +8,7 @@
 #include "dkv_internal.h"
 
 #include <algorithm>
+#include <cmath>
 
 namespace dkv {
 
@@ -298,23 +299,59 @@ DKV_DEVICE void rope_vec(uint4& v, const float* cs, int half, int k0) {
 struct RopeArgs {
   const void* src[3];
   void* dst[3];
-  int64_t heads[3];  // 0: tensor absent
+  int64_t nvec[3];   // 16-byte vectors per row of each tensor (0: tensor absent)
   int rotate[3];
   int64_t head_dim;
   const int64_t* positions;
   const int64_t* idx;
-  double base;
+  double log2_base;
   int inverse;
 };
+
+// Every thread issues its (up to kVecPerThread) 16-byte loads of the row FIRST -- their addresses
+// depend only on the gather index -- and computes the row's angles while they are in flight.
+constexpr int kRopeVecPerThread = 3;
 
 template <typename T>
 __global__ void rope_rows_kernel(const RopeArgs a) {
   extern __shared__ float cs[];  // [d/2] cos, [d/2] sin
   const int64_t r = blockIdx.x;
   const int half = static_cast<int>(a.head_dim / 2);
+  constexpr int kPairs = sizeof(T) == 2 ? 4 : 2;  // pairs per 16-byte vector
+  const int64_t sr = a.idx ? a.idx[r] : r;
+  const int n0 = static_cast<int>(a.nvec[0]), n1 = static_cast<int>(a.nvec[1]), n2 = static_cast<int>(a.nvec[2]);
+  const int n01 = n0 + n1, total = n01 + n2;
+  // vector i of the row -> (tensor, offset); pointers chosen by selects (a runtime index into
+  // the parameter arrays would copy them to local memory)
+  struct Loc {
+    const uint4* src;
+    uint4* dst;
+    int off;
+    bool rot;
+  };
+  auto locate = [&](int i) {
+    Loc l;
+    if (i < n0) {
+      l = {reinterpret_cast<const uint4*>(a.src[0]) + sr * n0, reinterpret_cast<uint4*>(a.dst[0]) + r * n0, i,
+           a.rotate[0] != 0};
+    } else if (i < n01) {
+      l = {reinterpret_cast<const uint4*>(a.src[1]) + sr * n1, reinterpret_cast<uint4*>(a.dst[1]) + r * n1, i - n0,
+           a.rotate[1] != 0};
+    } else {
+      l = {reinterpret_cast<const uint4*>(a.src[2]) + sr * n2, reinterpret_cast<uint4*>(a.dst[2]) + r * n2,
+           i - n01, a.rotate[2] != 0};
+    }
+    return l;
+  };
+  uint4 v[kRopeVecPerThread];
+#pragma unroll
+  for (int j = 0; j < kRopeVecPerThread; ++j) {
+    const int i = threadIdx.x + j * blockDim.x;
+    if (i < total) v[j] = __ldg(locate(i).src + locate(i).off);
+  }
   const double pos = static_cast<double>(a.positions[r]);
   for (int k = threadIdx.x; k < half; k += blockDim.x) {
-    const double inv_freq = exp2(-2.0 * k / static_cast<double>(a.head_dim) * log2(a.base));
+    const double inv_freq = exp2(-2.0 * k / static_cast<double>(a.head_dim) * a.log2_base);
     double ang = pos * inv_freq;
     ang -= 6.283185307179586 * rint(ang * 0.15915494309189535);  // to [-pi, pi]
     float sf, cf;
@@ -323,20 +360,23 @@ __global__ void rope_rows_kernel(const RopeArgs a) {
     cs[half + k] = a.inverse ? -sf : sf;
   }
   __syncthreads();
-  const int64_t sr = a.idx ? a.idx[r] : r;
-  constexpr int kPairs = sizeof(T) == 2 ? 4 : 2;  // pairs per 16-byte vector
 #pragma unroll
-  for (int t = 0; t < 3; ++t) {
-    if (a.heads[t] == 0) continue;
-    const int64_t nvec = a.heads[t] * half / kPairs;
-    const uint4* in = reinterpret_cast<const uint4*>(static_cast<const T*>(a.src[t]) + sr * a.heads[t] * a.head_dim);
-    uint4* out = reinterpret_cast<uint4*>(static_cast<T*>(a.dst[t]) + r * a.heads[t] * a.head_dim);
-    for (int64_t i = threadIdx.x; i < nvec; i += blockDim.x) {
-      uint4 v = in[i];
-      if (a.rotate[t]) rope_vec<T>(v, cs, half, static_cast<int>((i * kPairs) % half));
-      out[i] = v;
+  for (int j = 0; j < kRopeVecPerThread; ++j) {
+    const int i = threadIdx.x + j * blockDim.x;
+    if (i < total) {
+      const Loc l = locate(i);
+      if (l.rot) rope_vec<T>(v[j], cs, half, (l.off * kPairs) % half);
+      l.dst[l.off] = v[j];
     }
-  }}
+  }
+  // rows wider than kRopeVecPerThread x blockDim vectors (not hit by the launch below)
+  for (int i = threadIdx.x + kRopeVecPerThread * blockDim.x; i < total; i += blockDim.x) {
+    const Loc l = locate(i);
+    uint4 w = l.src[l.off];
+    if (l.rot) rope_vec<T>(w, cs, half, (l.off * kPairs) % half);
+    l.dst[l.off] = w;
+  }
+}
 
 extern "C" int32_t dkv_rope_qkv_rows(const void* q_src, const void* k_src, const void* v_src, void* q_dst,
                                      void* k_dst, void* v_dst, int32_t dtype, int64_t n_rows, int64_t heads,
@@ -352,7 +392,7 @@ extern "C" int32_t dkv_rope_qkv_rows(const void* q_src, const void* k_src, const
   const void* srcs[3] = {q_src, k_src, v_src};
   void* dsts[3] = {q_dst, k_dst, v_dst};
   const int64_t hs[3] = {heads, kv_heads, kv_heads};
-  int64_t maxvec = 0;
+  int64_t total = 0;
   for (int t = 0; t < 3; ++t) {
     if (!srcs[t] && !dsts[t]) continue;
     if (!srcs[t] || !dsts[t] || hs[t] <= 0 || (srcs[t] == dsts[t] && idx) ||
@@ -362,23 +402,26 @@ extern "C" int32_t dkv_rope_qkv_rows(const void* q_src, const void* k_src, const
     }
     a.src[t] = srcs[t];
     a.dst[t] = dsts[t];
-    a.heads[t] = hs[t];
+    a.nvec[t] = hs[t] * head_dim / 2 / pairs_per_vec;
     a.rotate[t] = t < 2;
-    maxvec = std::max<int64_t>(maxvec, hs[t] * head_dim / 2 / pairs_per_vec);
+    total += a.nvec[t];
   }
   if ((head_dim / 2) % pairs_per_vec) {
     set_error("dkv_rope_qkv_rows: head_dim must be a multiple of 8 (bf16) / 4 (fp32)");
     return DKV_ERR_UNSUPPORTED;
   }
-  if (n_rows == 0 || maxvec == 0) return DKV_OK;
+  if (n_rows == 0 || total == 0) return DKV_OK;
   a.head_dim = head_dim;
   a.positions = positions;
   a.idx = idx;
-  a.base = base;
+  a.log2_base = std::log2(base);
   a.inverse = inverse;
   auto st = static_cast<cudaStream_t>(stream);
   const size_t sm = static_cast<size_t>(head_dim) * sizeof(float);
-  const int threads = maxvec >= 256 ? 256 : (maxvec >= 128 ? 128 : 64);
+  // enough threads that every vector of the row is one of the up-front loads (<= 1024)
+  int64_t want = (total + kRopeVecPerThread - 1) / kRopeVecPerThread;
+  want = std::max<int64_t>(want, head_dim / 2);
+  const int threads = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(256, (want + 31) / 32 * 32)));
   if (dtype == DKV_BF16)
     rope_rows_kernel<__nv_bfloat16><<<static_cast<unsigned>(n_rows), threads, sm, st>>>(a);
   else
