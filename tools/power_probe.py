@@ -33,7 +33,7 @@ def sampler():
         time.sleep(0.02)
 th = threading.Thread(target=sampler); th.start()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-reps = 60
+reps = int(os.environ.get("REPS", "60"))
 e0.record()
 for _ in range(reps):
     run()
