@@ -70,6 +70,7 @@ struct Params {
   int num_seqs, total_q, ctx_len, heads, kv_heads, group, tq;
   int n_main_items;       // items >= n_main_items are Call 1 items (causal self-attention over the prompt)
   float scale_log2;       // softmax_scale * log2(e)
+  int ablate;             // timing experiments only (DKV_FWD_ABLATE): 1 K/V loads, 2 exponentials
 };
 
 struct Smem {
@@ -208,13 +209,14 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         const int row = is_ctx ? j * kBN : seq0 + j * kBN;
         mbar_wait(&sm.k_empty[slot], ph ^ 1);
         TRACE(T_Q_LOAD, it);
-        mbar_arrive_expect_tx(&sm.k_full[slot], C::kTileBytes);
-        for (int pn = 0; pn < C::kPanels; ++pn)
+        const bool skip_kv = (p.ablate & 1) || ((p.ablate & 4) && it >= C::kStages);  // 4: reuse the first tiles
+        mbar_arrive_expect_tx(&sm.k_full[slot], skip_kv ? 0 : C::kTileBytes);
+        for (int pn = 0; pn < C::kPanels && !skip_kv; ++pn)
           tma_load_3d_hint(sK + slot * C::kTileBytes + pn * C::kPanelBytes, mk, &sm.k_full[slot], pn * 64, hk,
                            row, pol_kv);
         mbar_wait(&sm.v_empty[slot], ph ^ 1);
-        mbar_arrive_expect_tx(&sm.v_full[slot], C::kTileBytes);
-        for (int pn = 0; pn < C::kPanels; ++pn)
+        mbar_arrive_expect_tx(&sm.v_full[slot], skip_kv ? 0 : C::kTileBytes);
+        for (int pn = 0; pn < C::kPanels && !skip_kv; ++pn)
           tma_load_3d_hint(sV + slot * C::kTileBytes + pn * C::kPanelBytes, mv, &sm.v_full[slot], pn * 64, hk,
                            row, pol_kv);
       }
@@ -381,7 +383,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
           for (int i = 0; i < 16; ++i) {
             const float2 x = __ffma2_rn(make_float2(s[c0 + 2 * i], s[c0 + 2 * i + 1]), sc2, nm2);
             float2 e;
-            if (i >= 16 - kPolyPairs) {
+            if (p.ablate & 2) {
+              e = x;
+            } else if (i >= 16 - kPolyPairs) {
               e = ex2_poly2(x);
             } else {
               e.x = ex2(x.x);
@@ -491,6 +495,10 @@ int launch(const SimtArgs& a, const CtxSelf* self, cudaStream_t st) {
   p.group = G;
   p.tq = tq;
   p.scale_log2 = a.scale * 1.4426950408889634f;
+  {
+    const char* e = getenv("DKV_FWD_ABLATE");
+    p.ablate = e ? atoi(e) : 0;
+  }
   const int blocks_per_seq = a.total_q > 0 ? (a.max_seqlen + 2 * tq - 1) / (2 * tq) : 0;
   const int64_t main_items = static_cast<int64_t>(blocks_per_seq) * a.num_seqs * a.kv_heads;
   const int64_t self_items =
