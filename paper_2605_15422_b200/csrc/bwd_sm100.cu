@@ -87,7 +87,8 @@ struct Params {
   int num_seqs, total_q, ctx_len, heads, kv_heads, group, tq, tpad;
   int chunk, n_ctx_items, n_ctx_tiles;
   int atomic_ctx;
-  int ablate;  // timing experiments only (DKV_BWD_ABLATE): 1 drain I/O, 2 compute math, 4 Q/dO loads
+  int ablate;  // timing experiments only (DKV_BWD_ABLATE): 1 drain I/O, 2 compute math, 4 Q/dO loads,
+               // 8 the additive-constant MMAs
   float scale, scale_log2;
 };
 
@@ -307,11 +308,11 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) mma_ss(tS, dKk + koff_kv(k), dQk + koff_q(k), id_sdp, k > 0);
           // S^T[k][c] += -lse[c] / scale  (so that P = exp2(S'^T * scale * log2 e))
-          mma_ss(tS, dOnes, dX, id_sdp, 1u);
+          if (!(p.ablate & 8)) mma_ss(tS, dOnes, dX, id_sdp, 1u);
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) mma_ss(tdP, dVk + koff_kv(k), dOk + koff_q(k), id_sdp, k > 0);
           // dP^T[k][c] += -D[c]  (so that dS^T = P^T * dP'^T)
-          mma_ss(tdP, dOnes, dX + (kXBytes >> 4), id_sdp, 1u);
+          if (!(p.ablate & 8)) mma_ss(tdP, dOnes, dX + (kXBytes >> 4), id_sdp, 1u);
           mma_commit(&bar.sdp_full);
         }
         if (i > 0) {
