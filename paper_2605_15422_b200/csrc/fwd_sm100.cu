@@ -22,7 +22,8 @@
 //     with lazy O rescaling (only when the running max grows by > 8).
 //   * Roles: warps 0-7 softmax(A), 8-15 softmax(B) -- two warps per TMEM lane quadrant, one
 //     per 64-key half of each row --, 16 TMA producer + TMEM allocator, 17 MMA issuer
-//     (setmaxnreg: 112 registers for softmax warps, 56 for warpgroup 4).
+//     (18 warps = 5 on some SM sub-partitions, whose 16K registers cap them at 96 per thread;
+//     a setmaxnreg split was measured to deadlock or spill).
 #include "dkv_internal.h"
 #include "tma_host.h"
 #include "trace.cuh"
@@ -34,16 +35,9 @@ namespace fwd {
 
 constexpr int kBM = 128;  // rows per Q tile
 constexpr int kBN = 128;  // keys per KV tile
-constexpr int kThreads = 640;  // 16 softmax warps, producer, MMA issuer, 2 idle (warpgroup 4)
+constexpr int kThreads = 576;  // 16 softmax warps, producer, MMA issuer
 constexpr int kWProd = 16, kWMma = 17;
-constexpr int kRegsSoftmax = 112, kRegsOther = 56;  // setmaxnreg split (launch: 96 per thread)
-#ifndef FWD_SETMAXNREG
-#define FWD_SETMAXNREG 0  // 1 deadlocks (5 warps per sub-partition); the softmax fits 96 registers
-#endif
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-#ifndef FWD_ALTERNATE
-#define FWD_ALTERNATE 0  // strict A/B alternation measured slower (9.3 vs 8.6 ms at C3)
-#endif
 #ifndef FWD_POLY
 #define FWD_POLY 5
 #endif
@@ -77,7 +71,6 @@ struct Smem {
   uint64_t q_full;
   uint64_t k_full[4], k_empty[4], v_full[4], v_empty[4];
   uint64_t s_full[2], p_full[2], o_full[2];
-  uint64_t turn[2];  // FWD_ALTERNATE: turn[t] = the other tile's softmax finished this round
   uint32_t tmem_base;
   // the two column halves of a row exchange partial row maxima (and, at the end, row sums)
   float xch[2][2][2][128];  // [tile][iteration parity][column half][row]
@@ -154,7 +147,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
       mbar_init(&sm.s_full[i], 1);
       mbar_init(&sm.p_full[i], 256);
       mbar_init(&sm.o_full[i], 1);
-      mbar_init(&sm.turn[i], 256);
     }
     fence_mbar_init();
   }
@@ -183,7 +175,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
 
   if (warp == kWProd) {
     // ================= TMA producer
-    if (FWD_SETMAXNREG) regs_dec<kRegsOther>();
     if (elect_one()) {
       tma_prefetch(mq);
       tma_prefetch(mk_own);
@@ -228,7 +219,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     tmem_dealloc<512>(tmem);
   } else if (warp == kWMma) {
     // ================= MMA issuer (one thread)
-    if (FWD_SETMAXNREG) regs_dec<kRegsOther>();
     if (elect_one()) {
       const uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, false, false);
       const uint32_t idesc_o = idesc_bf16_f32(kBM, D, false, true);
@@ -286,9 +276,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     }
     __syncwarp();
     done();
-  } else if (warp > kWMma) {
-    if (FWD_SETMAXNREG) regs_dec<kRegsOther>();  // idle warps 18-19 complete warpgroup 4's register hand-back
-    done();
   } else {
     // ================= softmax: two warps per row quadrant and tile, thread = one row x 64
     // keys (column half h).  One warp per sub-partition is latency-bound (tools/trace_fwd.py:
@@ -310,7 +297,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     const int qmin = tok0 + t * p.tq;                  // first token of the tile
     const int cb = 64 * h;                             // first key column of this half
     constexpr int kDH = D / 2;                         // O columns this half rescales / stores
-    if (FWD_SETMAXNREG) regs_inc<kRegsSoftmax>();
     float m_run = -INFINITY, l_run = 0.f;
     if (tile_ok) {
       for (int it = 0; it < n_iter; ++it) {
@@ -329,15 +315,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
           for (int i = 0; i < 64; ++i) s[i] = __uint_as_float(u[i]);
         }
         if (threadIdx.x == 0) TRACE(T_C_DP, it);
-#if FWD_ALTERNATE
-        // strict A/B alternation of the two tiles' softmax: each then has the sub-partitions'
-        // MUFU pipes to itself (~half the time of two overlapping) and hides under the other
-        // tile's MMAs.  A waits for B's previous round, B for A's current one.
-        if (has_b) {
-          if (t == 0 && it > 0) mbar_wait(&sm.turn[0], (it - 1) & 1);
-          if (t == 1) mbar_wait(&sm.turn[1], it & 1);
-        }
-#endif
         // masks: own tiles on/after the tile's first token are causal; the last
         // context tile may be partial (keys >= P are out of bounds)
         const int kbase = j * kBN + cb;
@@ -421,9 +398,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         tc_fence_before();
         mbar_arrive(&sm.p_full[t]);
         if (threadIdx.x == 0) TRACE(T_C_P, it);
-#if FWD_ALTERNATE
-        if (has_b) mbar_arrive(&sm.turn[t ^ 1]);
-#endif
       }
       // ---- epilogue: l = both halves' partial sums; O / l -> bf16 (each half D/2 columns), lse
       sm.xch[t][n_iter & 1][h][row] = l_run;
