@@ -326,14 +326,16 @@ def main():
     def fwd_only():
         saved["oc"], saved["lc"], saved["od"], saved["ld"] = dkv.dualkv_two_call_fwd(qc, dec0)
 
-    fwd_only()  # warm the allocator for this call pattern before timing it
+    for _ in range(2):  # warm the allocator for this call pattern (two live output sets) before timing it
+        fwd_only()
     fwd_ms = timed(fwd_only, args.steps)
 
     def bwd_only():
         dkv.dualkv_two_call_bwd(qc, dec0, saved["oc"], saved["lc"], doc, saved["od"], saved["ld"], dod0,
                                 deterministic=False)
 
-    bwd_only()
+    for _ in range(2):
+        bwd_only()
     bwd_ms = timed(bwd_only, args.steps)
     clocks.pause()
     ctx_b = dkv.VarlenBatch(qc, kc, vc, np.array([0, p]))

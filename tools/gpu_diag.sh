@@ -1,3 +1,2 @@
-timeout 300 python -m pytest tests/test_gpu_parity.py tests/test_gpu_properties.py tests/test_gpu_twocall.py -x -q -p no:cacheprovider 2>&1 | tail -2
-for L in libdkv.so libdkv_old.so libdkv.so libdkv_old.so libdkv.so libdkv_old.so; do echo -n "$L "; DKV_LIB=$L REPS=250 timeout 200 python tools/power_probe.py fwd; done
-for i in 1 2; do for L in libdkv.so libdkv_old.so; do DKV_LIB=$L timeout 100 python tools/time_fwd.py; done; done
+for L in libdkv.so libdkv_old.so libdkv.so libdkv_old.so; do echo -n "$L "; DKV_LIB=$L timeout 600 python bench.py --no-cpu --no-e2e --no-replicated 2>&1 | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], 'fwd', d['fwd_ms_group0'], 'bwd', d['bwd_ms_group0'], d['roofline']['kernel_ms'], d['clocks']['sm_mhz'])"; done
