@@ -623,11 +623,8 @@ int launch_tc_bwd2(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, 
     set_error("backward grid too large");
     return DKV_ERR_UNSUPPORTED;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dualkv_bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    attr = true;
-  }
+  if (!ensure_smem_optin(reinterpret_cast<const void*>(dualkv_bwd2_kernel), kSmemBytes, "dualkv_bwd2_kernel"))
+    return DKV_ERR_CUDA;
   dualkv_bwd2_kernel<<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(p);
   return DKV_OK;
 }

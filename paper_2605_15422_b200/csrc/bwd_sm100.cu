@@ -625,11 +625,8 @@ int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, c
     set_error("backward grid too large");
     return DKV_ERR_UNSUPPORTED;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dualkv_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    attr = true;
-  }
+  if (!ensure_smem_optin(reinterpret_cast<const void*>(dualkv_bwd_kernel), kSmemBytes, "dualkv_bwd_kernel"))
+    return DKV_ERR_CUDA;
   dualkv_bwd_kernel<<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(p);
   return DKV_OK;
 }

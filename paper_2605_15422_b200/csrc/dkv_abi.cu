@@ -7,6 +7,8 @@
 // G | 128) or the fp32 SIMT kernels, all stream-ordered on `stream`.
 #include <algorithm>
 #include <cstdio>
+#include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -18,6 +20,25 @@ namespace dkv {
 
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+
+bool ensure_smem_optin(const void* kernel, int bytes, const char* name) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    set_error(std::string(name) + ": cudaGetDevice failed");
+    return false;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({kernel, dev})) return true;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) {
+    set_error(std::string(name) + ": cudaFuncSetAttribute(max dynamic smem) failed: " + cudaGetErrorString(e));
+    return false;
+  }
+  done.insert({kernel, dev});
+  return true;
+}
 
 // ---- profiling hooks (bench harness only; off by default)
 struct ProfState {

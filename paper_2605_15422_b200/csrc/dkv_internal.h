@@ -35,6 +35,10 @@ struct SimtArgs {
 
 void set_error(const std::string& msg);
 
+// Opt a kernel into `bytes` of dynamic shared memory on the CURRENT device, once per
+// (kernel, device); thread-safe.  Returns false (error recorded) if the driver refuses.
+bool ensure_smem_optin(const void* kernel, int bytes, const char* name);
+
 // Call 1 of the two-call decomposition fused into a Call 2 launch: the prompt's own queries
 // (rows [0, ctx_len) of q/out/dout/dq below) attend causally to the context keys.
 struct CtxSelf {

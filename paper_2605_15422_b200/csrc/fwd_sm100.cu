@@ -484,11 +484,8 @@ int launch(const SimtArgs& a, const CtxSelf* self, cudaStream_t st) {
     return DKV_ERR_UNSUPPORTED;
   }
   p.n_main_items = static_cast<int>(main_items);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(dualkv_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    attr_set = true;
-  }
+  if (!ensure_smem_optin(reinterpret_cast<const void*>(dualkv_fwd_kernel<D>), C::kSmemBytes, "dualkv_fwd_kernel"))
+    return DKV_ERR_CUDA;
   dualkv_fwd_kernel<D><<<static_cast<unsigned>(grid), kThreads, C::kSmemBytes, st>>>(p);
   return DKV_OK;
 }
