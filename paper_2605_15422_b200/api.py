@@ -85,7 +85,8 @@ def _device_offsets(host: np.ndarray) -> torch.Tensor:
     dev = _CU_CACHE.get(key)
     if dev is None:
         if len(_CU_CACHE) >= 256:  # rare: drop the cache once no kernel can still read it
-            torch.cuda.synchronize()
+            for d in {k[0] for k in _CU_CACHE}:
+                torch.cuda.synchronize(d)
             _CU_CACHE.clear()
         dev = torch.as_tensor(host.astype(np.int32), device="cuda")
         _CU_CACHE[key] = dev
