@@ -51,11 +51,19 @@ struct Cfg {
   static constexpr int kStages = D == 128 ? 2 : 3; // K ring and V ring depth
   static constexpr int kSmemTiles = (2 + 2 * kStages) * kTileBytes;
   static constexpr int kSmemBytes = kSmemTiles + 8192 /*barriers + row-max exchange*/ + 1024 /*align slack*/;
+  // CTA-pair mode (D = 128): each CTA holds half of every K tile (64 keys, two 64-column panels)
+  // and half of every V tile (all 128 keys, 64 of the d columns)
+  static constexpr int kKHalf = 64 * D * 2;
+  static constexpr int kVHalf = kBN * 64 * 2;
+  static constexpr int kPairStages = 4;
+  static constexpr int kSmemTilesPair = 2 * kTileBytes + kPairStages * (kKHalf + kVHalf);
+  static constexpr int kSmemBytesPair = kSmemTilesPair + 8192 + 1024;
 };
 
 struct Params {
   CUtensorMap tm_q, tm_k, tm_v, tm_kc, tm_vc;
   CUtensorMap tm_qs;      // fused Call 1: the prompt's own queries [P, H, d]
+  CUtensorMap tm_k64, tm_kc64;  // pair mode: K boxes of 64 keys (each CTA loads one half)
   __nv_bfloat16* out;
   float* lse;
   __nv_bfloat16* out_s;   // fused Call 1 outputs [P, H, d], lse [H, P]
@@ -76,28 +84,38 @@ struct Smem {
   float xch[2][2][2][128];  // [tile][iteration parity][column half][row]
 };
 
-template <int D>
+// kPair: a 2-CTA cluster runs FOUR Q tiles (two per CTA) through M = 256 tcgen05 MMAs issued by
+// the leader (cta_group::2): each CTA loads only half of every K tile (64 keys) and half of
+// every V tile (64 d columns), so K/V traffic into the SMs and the B-operand shared-memory
+// reads per FLOP halve; S, P and O stay in each CTA's own tensor memory.
+template <int D, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
+  static_assert(!kPair || D == 128, "pair mode is laid out for d = 128");
+  constexpr int kSt = kPair ? C::kPairStages : C::kStages;
+  constexpr int kKBytes = kPair ? C::kKHalf : C::kTileBytes;  // per K stage
+  constexpr int kVBytes = kPair ? C::kVHalf : C::kTileBytes;  // per V stage
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ[2] = {base, base + C::kTileBytes};
   uint8_t* sK = base + 2 * C::kTileBytes;
-  uint8_t* sV = sK + C::kStages * C::kTileBytes;
-  Smem& sm = *reinterpret_cast<Smem*>(base + C::kSmemTiles);
+  uint8_t* sV = sK + kSt * kKBytes;
+  Smem& sm = *reinterpret_cast<Smem*>(base + (kPair ? C::kSmemTilesPair : C::kSmemTiles));
+  const uint32_t crank = kPair ? cluster_ctarank() : 0;  // 0: the pair's leader (issues the MMAs)
+  const int item = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
 
   // ---- work item.  Main items: (q-block pair counted from the sequence end, sequence, kv head)
   // of the two-region problem.  Fused Call 1 items (two-call launch only): the prompt's own
   // queries attend causally to the prompt keys -- one more "sequence" whose own-region K/V are
   // the context tensors and which has no context region.
-  const bool self_item = static_cast<int>(blockIdx.x) >= p.n_main_items;
+  const bool self_item = item >= p.n_main_items;
   int hk, jb, seq0, rlen, n_ctx, lse_stride;
   const CUtensorMap *mq, *mk_own, *mv_own;
   __nv_bfloat16* out;
   float* lse_out;
   if (!self_item) {
-    hk = blockIdx.x % p.kv_heads;
-    const int rest = blockIdx.x / p.kv_heads;
+    hk = item % p.kv_heads;
+    const int rest = item / p.kv_heads;
     const int seq = rest % p.num_seqs;
     jb = rest / p.num_seqs;
     seq0 = p.cu[seq];
@@ -110,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     lse_out = p.lse;
     lse_stride = p.total_q;
   } else {
-    const int b = blockIdx.x - p.n_main_items;
+    const int b = item - p.n_main_items;
     hk = b % p.kv_heads;
     jb = b / p.kv_heads;
     seq0 = 0;
@@ -123,12 +141,15 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     lse_out = p.lse_s;
     lse_stride = p.ctx_len;
   }
-  const int pair_tok = 2 * p.tq;
-  const int nblk = (rlen + pair_tok - 1) / pair_tok;
-  if (jb >= nblk) return;
-  const int tok0 = (nblk - 1 - jb) * pair_tok;  // first token of tile A (sequence-local)
-  const bool has_b = tok0 + p.tq < rlen;
-  const int last_tok = min(tok0 + pair_tok, rlen) - 1;
+  const int span_tok = (kPair ? 4 : 2) * p.tq;  // tokens of the item (two or four Q tiles)
+  const int nblk = (rlen + span_tok - 1) / span_tok;
+  if (jb >= nblk) return;  // (both CTAs of a pair: same item)
+  const int tok_item = (nblk - 1 - jb) * span_tok;
+  const int tok0 = tok_item + static_cast<int>(crank) * 2 * p.tq;  // first token of this CTA's tile A
+  // pair mode always runs both tiles (the leader's M = 256 MMAs cover both CTAs); rows past the
+  // sequence end are computed on zero / foreign rows and never stored
+  const bool has_b = kPair || tok0 + p.tq < rlen;
+  const int last_tok = min(tok_item + span_tok, rlen) - 1;  // the item's walk: the whole cluster
   const int n_own = last_tok / kBN + 1;
   const int n_iter = n_own + n_ctx;
 
@@ -137,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
 
   if (threadIdx.x == 0) {
     mbar_init(&sm.q_full, 1);
-    for (int i = 0; i < C::kStages; ++i) {
+    for (int i = 0; i < kSt; ++i) {
       mbar_init(&sm.k_full[i], 1);
       mbar_init(&sm.k_empty[i], 1);
       mbar_init(&sm.v_full[i], 1);
@@ -145,14 +166,20 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.s_full[i], 1);
-      mbar_init(&sm.p_full[i], 256);
+      mbar_init(&sm.p_full[i], kPair ? 16 : 256);  // pair: one arrival per softmax warp of both CTAs
       mbar_init(&sm.o_full[i], 1);
     }
     fence_mbar_init();
   }
-  if (warp == kWProd) tmem_alloc<512>(&sm.tmem_base);
+  if (warp == kWProd) {
+    if constexpr (kPair)
+      tmem_alloc2<512>(&sm.tmem_base);
+    else
+      tmem_alloc<512>(&sm.tmem_base);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPair) cluster_sync();  // the leader's barriers exist before any 2-SM TMA / arrive
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
@@ -168,9 +195,13 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
 
   // teardown without a common tail (each role keeps its own register budget to the end): all
   // warps arrive on barrier 15 when done with TMEM; the allocating warp waits there and frees it
+  // (pair mode: a cluster barrier phase instead, so neither CTA frees the pair's TMEM early)
   auto done = [&]() {
     tc_fence_before();
-    named_bar_arrive(15, kThreads);
+    if constexpr (kPair)
+      cluster_arrive();
+    else
+      named_bar_arrive(15, kThreads);
   };
 
   if (warp == kWProd) {
@@ -184,22 +215,45 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         tma_prefetch(&p.tm_vc);
       }
       const uint64_t pol_kv = policy_evict_last();
-      const int qbytes = C::kPanelBytes * C::kPanels * (has_b ? 2 : 1);
-      mbar_arrive_expect_tx(&sm.q_full, qbytes);
-      for (int t = 0; t < (has_b ? 2 : 1); ++t)
-        for (int pn = 0; pn < C::kPanels; ++pn)
-          tma_load_3d(sQ[t] + pn * C::kPanelBytes, mq, &sm.q_full, pn * 64, hk * p.group,
-                      seq0 + tok0 + t * p.tq);
+      if constexpr (kPair) {
+        if (crank == 0) mbar_arrive_expect_tx(&sm.q_full, 4 * C::kTileBytes);
+        const uint32_t lq = mapa_shared(&sm.q_full, 0);
+        for (int t = 0; t < 2; ++t)
+          for (int pn = 0; pn < C::kPanels; ++pn)
+            tma_load_3d_2sm(sQ[t] + pn * C::kPanelBytes, mq, lq, pn * 64, hk * p.group, seq0 + tok0 + t * p.tq);
+      } else {
+        const int qbytes = C::kPanelBytes * C::kPanels * (has_b ? 2 : 1);
+        mbar_arrive_expect_tx(&sm.q_full, qbytes);
+        for (int t = 0; t < (has_b ? 2 : 1); ++t)
+          for (int pn = 0; pn < C::kPanels; ++pn)
+            tma_load_3d(sQ[t] + pn * C::kPanelBytes, mq, &sm.q_full, pn * 64, hk * p.group,
+                        seq0 + tok0 + t * p.tq);
+      }
       for (int it = 0; it < n_iter; ++it) {
         bool is_ctx;
         const int j = tile_of(it, is_ctx);
-        const int slot = it % C::kStages;
-        const uint32_t ph = (it / C::kStages) & 1;
+        const int slot = it % kSt;
+        const uint32_t ph = (it / kSt) & 1;
         const CUtensorMap* mk = is_ctx ? &p.tm_kc : mk_own;
         const CUtensorMap* mv = is_ctx ? &p.tm_vc : mv_own;
         const int row = is_ctx ? j * kBN : seq0 + j * kBN;
         mbar_wait(&sm.k_empty[slot], ph ^ 1);
         TRACE(T_Q_LOAD, it);
+        if constexpr (kPair) {
+          // this CTA's halves: keys [64 r, +64) of K, d columns [64 r, +64) of V; both counted
+          // on the leader's barriers
+          const CUtensorMap* mk64 = is_ctx ? &p.tm_kc64 : (self_item ? &p.tm_kc64 : &p.tm_k64);
+          if (crank == 0) mbar_arrive_expect_tx(&sm.k_full[slot], 2 * C::kKHalf);
+          const uint32_t lk = mapa_shared(&sm.k_full[slot], 0);
+          for (int pn = 0; pn < C::kPanels; ++pn)
+            tma_load_3d_2sm(sK + slot * C::kKHalf + pn * (C::kKHalf / 2), mk64, lk, pn * 64, hk,
+                            row + static_cast<int>(crank) * 64);
+          mbar_wait(&sm.v_empty[slot], ph ^ 1);
+          if (crank == 0) mbar_arrive_expect_tx(&sm.v_full[slot], 2 * C::kVHalf);
+          tma_load_3d_2sm(sV + slot * C::kVHalf, mv, mapa_shared(&sm.v_full[slot], 0), static_cast<int>(crank) * 64,
+                          hk, row);
+          continue;
+        }
         const bool skip_kv = (p.ablate & 1) || ((p.ablate & 4) && it >= C::kStages);  // 4: reuse the first tiles
         mbar_arrive_expect_tx(&sm.k_full[slot], skip_kv ? 0 : C::kTileBytes);
         for (int pn = 0; pn < C::kPanels && !skip_kv; ++pn)
@@ -214,62 +268,89 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     }
     __syncwarp();
     tc_fence_before();
-    named_bar_sync(15, kThreads);
-    tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    if constexpr (kPair) {
+      cluster_arrive();
+      cluster_wait();  // every thread of both CTAs is done with the pair's TMEM
+      tc_fence_after();
+      tmem_dealloc2<512>(tmem);
+    } else {
+      named_bar_sync(15, kThreads);
+      tc_fence_after();
+      tmem_dealloc<512>(tmem);
+    }
   } else if (warp == kWMma) {
     // ================= MMA issuer (one thread)
-    if (elect_one()) {
-      const uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, false, false);
-      const uint32_t idesc_o = idesc_bf16_f32(kBM, D, false, true);
+    if ((!kPair || crank == 0) && elect_one()) {
+      constexpr int kM = kPair ? 2 * kBM : kBM;
+      const uint32_t idesc_s = idesc_bf16_f32(kM, kBN, false, false);
+      const uint32_t idesc_o = idesc_bf16_f32(kM, D, false, true);
       const uint32_t tS[2] = {tmem + 0, tmem + 128};
       const uint32_t tO[2] = {tmem + 256, tmem + 256 + 128};
       const int ntile = has_b ? 2 : 1;
       auto issue_s = [&](int t, int kslot) {
         const uint32_t qa = smem_u32(sQ[t]);
-        const uint32_t ka = smem_u32(sK + kslot * C::kTileBytes);
+        const uint32_t ka = smem_u32(sK + kslot * kKBytes);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * C::kPanelBytes + (k & 3) * 32;
-          mma_ss(tS[t], sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + off, 16, 1024), idesc_s, k > 0);
+          if constexpr (kPair) {
+            const uint32_t koff = (k >> 2) * (C::kKHalf / 2) + (k & 3) * 32;  // 64-row K panels
+            mma_ss2(tS[t], sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + koff, 16, 1024), idesc_s, k > 0);
+          } else {
+            mma_ss(tS[t], sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + off, 16, 1024), idesc_s, k > 0);
+          }
         }
       };
       auto issue_pv = [&](int t, int vslot, bool accum) {
-        const uint32_t va = smem_u32(sV + vslot * C::kTileBytes);
+        const uint32_t va = smem_u32(sV + vslot * kVBytes);
 #pragma unroll
-        for (int k = 0; k < kBN / 16; ++k)
-          mma_ts(tO[t], tS[t] + k * 8, sdesc_sw128(va + k * 2048, C::kPanelBytes, 1024), idesc_o,
-                 (accum || k > 0) ? 1u : 0u);
+        for (int k = 0; k < kBN / 16; ++k) {
+          if constexpr (kPair)
+            mma_ts2(tO[t], tS[t] + k * 8, sdesc_sw128(va + k * 2048, C::kPanelBytes, 1024), idesc_o,
+                    (accum || k > 0) ? 1u : 0u);
+          else
+            mma_ts(tO[t], tS[t] + k * 8, sdesc_sw128(va + k * 2048, C::kPanelBytes, 1024), idesc_o,
+                   (accum || k > 0) ? 1u : 0u);
+        }
+      };
+      auto commit = [&](uint64_t* bar) {
+        if constexpr (kPair)
+          mma_commit2_mc(bar);
+        else
+          mma_commit(bar);
       };
       mbar_wait(&sm.q_full, 0);
       mbar_wait(&sm.k_full[0], 0);
       tc_fence_after();
       for (int t = 0; t < ntile; ++t) {
         issue_s(t, 0);
-        mma_commit(&sm.s_full[t]);
+        commit(&sm.s_full[t]);
       }
-      mma_commit(&sm.k_empty[0]);
+      commit(&sm.k_empty[0]);
       for (int it = 0; it < n_iter; ++it) {
-        const int vslot = it % C::kStages;
-        const uint32_t vph = (it / C::kStages) & 1;
-        const int nslot = (it + 1) % C::kStages;
-        const uint32_t nph = ((it + 1) / C::kStages) & 1;
+        const int vslot = it % kSt;
+        const uint32_t vph = (it / kSt) & 1;
+        const int nslot = (it + 1) % kSt;
+        const uint32_t nph = ((it + 1) / kSt) & 1;
         const bool more = it + 1 < n_iter;
         mbar_wait(&sm.v_full[vslot], vph);
         if (more) mbar_wait(&sm.k_full[nslot], nph);
         for (int t = 0; t < ntile; ++t) {
-          mbar_wait(&sm.p_full[t], it & 1);
+          if constexpr (kPair)
+            mbar_wait_cluster(&sm.p_full[t], it & 1);  // arrivals from both CTAs
+          else
+            mbar_wait(&sm.p_full[t], it & 1);
           tc_fence_after();
           TRACE(t == 0 ? T_ISS_DV : T_ISS_DK, it);
           issue_pv(t, vslot, it > 0);
-          if (t == ntile - 1) mma_commit(&sm.v_empty[vslot]);
+          if (t == ntile - 1) commit(&sm.v_empty[vslot]);
           if (more) {
             TRACE(t == 0 ? T_ISS_S : T_ISS_DP, it + 1);
             issue_s(t, nslot);
-            mma_commit(&sm.s_full[t]);
-            if (t == ntile - 1) mma_commit(&sm.k_empty[nslot]);
+            commit(&sm.s_full[t]);
+            if (t == ntile - 1) commit(&sm.k_empty[nslot]);
           } else {
-            mma_commit(&sm.o_full[t]);
+            commit(&sm.o_full[t]);
           }
         }
       }
@@ -396,7 +477,17 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         if (threadIdx.x == 0) TRACE(T_MMA_END, it);
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&sm.p_full[t]);
+        if constexpr (kPair) {
+          __syncwarp();
+          if (lane == 0) {
+            if (crank == 0)
+              mbar_arrive(&sm.p_full[t]);
+            else
+              mbar_arrive_remote(mapa_shared(&sm.p_full[t], 0));
+          }
+        } else {
+          mbar_arrive(&sm.p_full[t]);
+        }
         if (threadIdx.x == 0) TRACE(T_C_P, it);
       }
       // ---- epilogue: l = both halves' partial sums; O / l -> bf16 (each half D/2 columns), lse
@@ -431,6 +522,15 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
   }
 }
 
+// DKV_FWD_PAIR=1: the CTA-pair (cta_group::2) forward for d = 128
+static bool fwd_pairs() {
+  static const bool v = [] {
+    const char* e = getenv("DKV_FWD_PAIR");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 template <int D>
 int launch(const SimtArgs& a, const CtxSelf* self, cudaStream_t st) {
   using C = Cfg<D>;
@@ -450,6 +550,12 @@ int launch(const SimtArgs& a, const CtxSelf* self, cudaStream_t st) {
       set_error("cuTensorMapEncodeTiled failed for k_ctx/v_ctx");
       return DKV_ERR_CUDA;
     }
+  }
+  const bool pair = D == 128 && fwd_pairs();
+  if (pair && ((a.total_q > 0 && !make_map_3d_bf16(&p.tm_k64, a.k, a.total_q, a.kv_heads, D, 1, 64)) ||
+               (a.ctx_len > 0 && !make_map_3d_bf16(&p.tm_kc64, a.k_ctx, a.ctx_len, a.kv_heads, D, 1, 64)))) {
+    set_error("cuTensorMapEncodeTiled failed for the pair-mode K maps");
+    return DKV_ERR_CUDA;
   }
   const bool with_self = self && a.ctx_len > 0;
   if (with_self && !make_map_3d_bf16(&p.tm_qs, self->q, a.ctx_len, a.heads, D, G, tq)) {
@@ -473,20 +579,43 @@ int launch(const SimtArgs& a, const CtxSelf* self, cudaStream_t st) {
     const char* e = getenv("DKV_FWD_ABLATE");
     p.ablate = e ? atoi(e) : 0;
   }
-  const int blocks_per_seq = a.total_q > 0 ? (a.max_seqlen + 2 * tq - 1) / (2 * tq) : 0;
+  const int span = (pair ? 4 : 2) * tq;  // tokens per work item (a CTA, or a CTA pair)
+  const int blocks_per_seq = a.total_q > 0 ? (a.max_seqlen + span - 1) / span : 0;
   const int64_t main_items = static_cast<int64_t>(blocks_per_seq) * a.num_seqs * a.kv_heads;
-  const int64_t self_items =
-      with_self ? static_cast<int64_t>((a.ctx_len + 2 * tq - 1) / (2 * tq)) * a.kv_heads : 0;
-  const int64_t grid = main_items + self_items;  // Call 1 items run in the tail of Call 2's
-  if (grid == 0) return DKV_OK;
-  if (grid > 0x7fffffff) {
+  const int64_t self_items = with_self ? static_cast<int64_t>((a.ctx_len + span - 1) / span) * a.kv_heads : 0;
+  const int64_t items = main_items + self_items;  // Call 1 items run in the tail of Call 2's
+  if (items == 0) return DKV_OK;
+  if (items * (pair ? 2 : 1) > 0x7fffffff) {
     set_error("forward grid too large");
     return DKV_ERR_UNSUPPORTED;
   }
   p.n_main_items = static_cast<int>(main_items);
-  if (!ensure_smem_optin(reinterpret_cast<const void*>(dualkv_fwd_kernel<D>), C::kSmemBytes, "dualkv_fwd_kernel"))
+  if (pair) {
+    const void* fn = reinterpret_cast<const void*>(dualkv_fwd_kernel<128, true>);
+    if (!ensure_smem_optin(fn, C::kSmemBytesPair, "dualkv_fwd_kernel(pair)")) return DKV_ERR_CUDA;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * items));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmemBytesPair;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, dualkv_fwd_kernel<128, true>, p);
+    if (e != cudaSuccess) {
+      set_error(std::string("forward pair launch failed: ") + cudaGetErrorString(e));
+      return DKV_ERR_CUDA;
+    }
+    return DKV_OK;
+  }
+  if (!ensure_smem_optin(reinterpret_cast<const void*>(dualkv_fwd_kernel<D, false>), C::kSmemBytes,
+                         "dualkv_fwd_kernel"))
     return DKV_ERR_CUDA;
-  dualkv_fwd_kernel<D><<<static_cast<unsigned>(grid), kThreads, C::kSmemBytes, st>>>(p);
+  dualkv_fwd_kernel<D, false><<<static_cast<unsigned>(items), kThreads, C::kSmemBytes, st>>>(p);
   return DKV_OK;
 }
 

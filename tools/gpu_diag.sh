@@ -1,1 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_large.py -x -q -p no:cacheprovider 2>&1 | tail -15
+for L in libdkv.so libdkv_old.so libdkv.so libdkv_old.so; do echo -n "$L "; DKV_LIB=$L REPS=250 timeout 200 python tools/power_probe.py fwd; done
