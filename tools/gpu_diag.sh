@@ -1,1 +1,1 @@
-for L in libdkv.so libdkv_old.so libdkv.so libdkv_old.so; do echo -n "$L "; DKV_LIB=$L REPS=250 timeout 200 python tools/power_probe.py fwd; done
+timeout 600 python -m pytest tests/test_gpu_variants.py -x -q -p no:cacheprovider 2>&1 | tail -3
