@@ -254,6 +254,21 @@ DKV_DEVICE void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
         : "memory");
   }
 }
+// polling wait without a suspend hint: a thread suspended in try_wait is woken late by arrivals
+// from a PEER CTA (remote mbarrier.arrive / 2-SM TMA complete_tx), ~1000 clk in
+// tools/trace_fwd.py; the pair's MMA issuer polls instead
+DKV_DEVICE void mbar_wait_poll(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
 template <int NCOLS>
 DKV_DEVICE void tmem_alloc2(uint32_t* smem_dst) {  // one warp in EACH CTA of the pair
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),

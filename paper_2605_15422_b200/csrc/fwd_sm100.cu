@@ -319,8 +319,15 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         else
           mma_commit(bar);
       };
-      mbar_wait(&sm.q_full, 0);
-      mbar_wait(&sm.k_full[0], 0);
+      // pair mode: these barriers complete from the peer CTA too -> poll (see mbar_wait_poll)
+      auto wait = [&](uint64_t* bar, uint32_t ph) {
+        if constexpr (kPair)
+          mbar_wait_poll(bar, ph);
+        else
+          mbar_wait(bar, ph);
+      };
+      wait(&sm.q_full, 0);
+      wait(&sm.k_full[0], 0);
       tc_fence_after();
       for (int t = 0; t < ntile; ++t) {
         issue_s(t, 0);
@@ -333,13 +340,10 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         const int nslot = (it + 1) % kSt;
         const uint32_t nph = ((it + 1) / kSt) & 1;
         const bool more = it + 1 < n_iter;
-        mbar_wait(&sm.v_full[vslot], vph);
-        if (more) mbar_wait(&sm.k_full[nslot], nph);
+        wait(&sm.v_full[vslot], vph);
+        if (more) wait(&sm.k_full[nslot], nph);
         for (int t = 0; t < ntile; ++t) {
-          if constexpr (kPair)
-            mbar_wait_cluster(&sm.p_full[t], it & 1);  // arrivals from both CTAs
-          else
-            mbar_wait(&sm.p_full[t], it & 1);
+          wait(&sm.p_full[t], it & 1);  // pair: arrivals from both CTAs
           tc_fence_after();
           TRACE(t == 0 ? T_ISS_DV : T_ISS_DK, it);
           issue_pv(t, vslot, it > 0);
@@ -489,6 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
           mbar_arrive(&sm.p_full[t]);
         }
         if (threadIdx.x == 0) TRACE(T_C_P, it);
+        if (threadIdx.x == 7 * 32) TRACE(T_D_END, it);  // the tile's last softmax warp (trace only)
       }
       // ---- epilogue: l = both halves' partial sums; O / l -> bf16 (each half D/2 columns), lse
       sm.xch[t][n_iter & 1][h][row] = l_run;
