@@ -241,9 +241,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DKV_BENCH_ONE_GPU=1 (test hook): every rank on cuda:0 over gloo, to exercise the
+    # multi-rank logic (ownership, barriers, max-over-ranks) on a one-GPU box
+    one_gpu = os.environ.get("DKV_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if one_gpu else "nccl")
     dev = torch.device("cuda", local)
     cfg = CONFIGS[args.config]
     p, h, hk, d = cfg["p"], cfg["h"], cfg["hk"], cfg["d"]
