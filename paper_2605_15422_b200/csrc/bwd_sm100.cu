@@ -44,7 +44,6 @@ namespace bwd {
 
 constexpr int kBK = 128;  // keys per tile (MMA M)
 constexpr int kBQ = 64;   // query rows per tile (MMA N for S^T / dP^T / dQ^T)
-constexpr int D = 128;
 constexpr int kThreads = 448;  // 8 compute warps, 4 dQ-drain warps, producer, MMA issuer
 constexpr int kWDrain = 8, kWProd = 12, kWMma = 13;
 constexpr int kDrainT0 = kWDrain * 32;  // first drain thread
@@ -53,24 +52,32 @@ constexpr int kDrainT0 = kWDrain * 32;  // first drain thread
 #endif
 constexpr int kPolyPairs = BWD_POLY;    // of every 16 exponential pairs, on the FMA pipe
 constexpr int kStages = 3;
-constexpr int kKVBytes = kBK * D * 2;       // 32 KB
-constexpr int kKVPanel = kBK * 128;         // 16 KB
-constexpr int kQBytes = kBQ * D * 2;        // 16 KB
-constexpr int kQPanel = kBQ * 128;          // 8 KB
+constexpr int kKVPanel = kBK * 128;         // 16 KB: one 64-column SW128 panel of a key tile
 constexpr int kPBytes = kBK * kBQ * 2;      // 16 KB
-constexpr int kOffK = 0;
-constexpr int kOffV = kOffK + kKVBytes;
-constexpr int kOffQ = kOffV + kKVBytes;
-constexpr int kOffDO = kOffQ + kStages * kQBytes;
-constexpr int kOffDS = kOffDO + kStages * kQBytes;
-constexpr int kXBytes = kBQ * 32;                     // [64 rows][16 bf16] SW32 tile (2 KB)
-constexpr int kOffX = kOffDS + kPBytes;               // per stage: -lse/scale tile, -D tile
-constexpr int kOffOnes = kOffX + kStages * 2 * kXBytes;  // [128 keys][16 bf16] SW32: 1,1,1,0...
-constexpr int kOffStage = kOffOnes + kBK * 32;        // dQ staging tile for the TMA reduce
-constexpr int kStageBytes = kBQ * D * 4;              // [64 rows][128 d] fp32 = 32 KB
-constexpr int kOffBar = kOffStage + kStageBytes;
-constexpr int kSmemBytes = kOffBar + 256 + 1024;
-static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory per block");
+constexpr int kXBytes = kBQ * 32;           // [64 rows][16 bf16] SW32 tile (2 KB)
+
+// Shared-memory layout for head dim D (64 or 128).  The K tile always has two panels: dQ^T =
+// K^T dS^T runs as an M=128 MMA over the head dim, so at D=64 the second panel holds zeros
+// (rows 64-127 of dQ^T come out zero and are not drained).
+template <int D>
+struct L {
+  static constexpr int kKBytes = kBK * 128 * 2;  // 32 KB (two panels)
+  static constexpr int kVBytes = kBK * D * 2;
+  static constexpr int kQBytes = kBQ * D * 2;
+  static constexpr int kQPanel = kBQ * 128;      // 8 KB
+  static constexpr int kOffK = 0;
+  static constexpr int kOffV = kOffK + kKBytes;
+  static constexpr int kOffQ = kOffV + kVBytes;
+  static constexpr int kOffDO = kOffQ + kStages * kQBytes;
+  static constexpr int kOffDS = kOffDO + kStages * kQBytes;
+  static constexpr int kOffX = kOffDS + kPBytes;               // per stage: -lse/scale tile, -D tile
+  static constexpr int kOffOnes = kOffX + kStages * 2 * kXBytes;  // [128 keys][16 bf16] SW32: 1,1,1,0...
+  static constexpr int kOffStage = kOffOnes + kBK * 32;        // dQ staging tile for the TMA reduce
+  static constexpr int kStageBytes = kBQ * D * 4;              // [64 rows][D] fp32
+  static constexpr int kOffBar = kOffStage + kStageBytes;
+  static constexpr int kSmemBytes = kOffBar + 256 + 1024;
+  static_assert(kSmemBytes <= 232448, "exceeds the 227 KB opt-in shared memory per block");
+};
 
 struct Params {
   CUtensorMap tm_q, tm_do, tm_k, tm_v, tm_kc, tm_vc, tm_dq;
@@ -134,7 +141,12 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
                : "memory");
 }
 
+template <int D>
 __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_constant__ Params p) {
+  using Y = L<D>;
+  constexpr int kQBytes = Y::kQBytes, kQPanel = Y::kQPanel, kStageBytes = Y::kStageBytes;
+  constexpr int kOffK = Y::kOffK, kOffV = Y::kOffV, kOffQ = Y::kOffQ, kOffDO = Y::kOffDO, kOffDS = Y::kOffDS;
+  constexpr int kOffX = Y::kOffX, kOffOnes = Y::kOffOnes, kOffStage = Y::kOffStage, kOffBar = Y::kOffBar;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars& bar = *reinterpret_cast<Bars*>(base + kOffBar);
@@ -230,6 +242,12 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     *reinterpret_cast<uint4*>(row + (1 ^ sw) * 16) = make_uint4(0u, 0u, 0u, 0u);
     fence_async_smem();
   }
+  if constexpr (D == 64) {
+    // the zero second panel of the key tile (head-dim rows 64-127 of K^T in the dQ^T MMA)
+    for (int i = threadIdx.x; i < kKVPanel / 16; i += kThreads)
+      reinterpret_cast<uint4*>(base + kOffK + kKVPanel)[i] = make_uint4(0u, 0u, 0u, 0u);
+    fence_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -247,8 +265,8 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       tma_prefetch(mx);
       tma_prefetch(mk);
       tma_prefetch(mv);
-      mbar_arrive_expect_tx(&bar.kv_full, 2 * kKVBytes);
-      for (int pn = 0; pn < 2; ++pn) {
+      mbar_arrive_expect_tx(&bar.kv_full, 2 * Y::kVBytes);
+      for (int pn = 0; pn < D / 64; ++pn) {
         tma_load_3d(base + kOffK + pn * kKVPanel, mk, &bar.kv_full, pn * 64, hk, kv_row0 + kbase);
         tma_load_3d(base + kOffV + pn * kKVPanel, mv, &bar.kv_full, pn * 64, hk, kv_row0 + kbase);
       }
@@ -263,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         TRACE(T_Q_LOAD, i);
         const int row0 = cu[it.s] + it.tok;
         mbar_arrive_expect_tx(&bar.q_full[st], ((p.ablate & 4) ? 0 : 2 * kQBytes) + 2 * kXBytes);
-        for (int pn = 0; pn < 2 && !(p.ablate & 4); ++pn) {
+        for (int pn = 0; pn < D / 64 && !(p.ablate & 4); ++pn) {
           tma_load_3d(base + kOffQ + st * kQBytes + pn * kQPanel, mq, &bar.q_full[st], pn * 64, hk * G, row0);
           tma_load_3d(base + kOffDO + st * kQBytes + pn * kQPanel, mdo, &bar.q_full[st], pn * 64, hk * G, row0);
         }
@@ -284,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       const uint32_t tdV = tmem + 256, tdK = tmem + 384;
       const uint32_t id_sdp = idesc_bf16_f32(kBK, kBQ, false, false);
       const uint32_t id_kv = idesc_bf16_f32(kBK, D, false, true);
-      const uint32_t id_dq = idesc_bf16_f32(D, kBQ, true, true);
+      const uint32_t id_dq = idesc_bf16_f32(128, kBQ, true, true);  // M = 128 head-dim rows (zeros past D)
       // descriptors built once; a K step adds its byte offset >> 4 to the start-address field
       const uint64_t dKk = sdesc_sw128(smem_u32(base + kOffK), 16, 1024);
       const uint64_t dVk = sdesc_sw128(smem_u32(base + kOffV), 16, 1024);
@@ -464,7 +482,8 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         if (threadIdx.x == kDrainT0) bulk_wait_read<1>();  // this half's previous reduce has read it
         named_bar_sync(1, 128);
 #pragma unroll
-        for (int c = 0; c < kBQ / 2; ++c) stg[c * D + d] = __uint_as_float(u[hh * (kBQ / 2) + c]);
+        for (int c = 0; c < kBQ / 2; ++c)
+          if (D == 128 || d < D) stg[c * D + d] = __uint_as_float(u[hh * (kBQ / 2) + c]);
         fence_async_smem();
         named_bar_sync(1, 128);
         if (threadIdx.x == kDrainT0) {
@@ -546,7 +565,7 @@ static bool use_v1() {
 }
 
 static bool tc_bwd1_supported(int head_dim, int heads, int kv_heads) {
-  if (head_dim != bwd::D || kv_heads <= 0 || heads % kv_heads) return false;
+  if ((head_dim != 64 && head_dim != 128) || kv_heads <= 0 || heads % kv_heads) return false;
   const int G = heads / kv_heads;
   return G <= bwd::kBQ && (bwd::kBQ % G) == 0;
 }
@@ -556,9 +575,9 @@ bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads) {
   return use_v1() ? tc_bwd1_supported(head_dim, heads, kv_heads) : tc_bwd2_supported(head_dim, heads, kv_heads);
 }
 
-int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, cudaStream_t st) {
-  if (!use_v1()) return launch_tc_bwd2(a, self, w, st);
-  using namespace bwd;
+namespace bwd {
+template <int D>
+static int launch(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, cudaStream_t st) {
   Params p{};
   const int G = a.heads / a.kv_heads;
   const int tq = kBQ / G;
@@ -625,10 +644,16 @@ int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, c
     set_error("backward grid too large");
     return DKV_ERR_UNSUPPORTED;
   }
-  if (!ensure_smem_optin(reinterpret_cast<const void*>(dualkv_bwd_kernel), kSmemBytes, "dualkv_bwd_kernel"))
+  if (!ensure_smem_optin(reinterpret_cast<const void*>(dualkv_bwd_kernel<D>), L<D>::kSmemBytes, "dualkv_bwd_kernel"))
     return DKV_ERR_CUDA;
-  dualkv_bwd_kernel<<<static_cast<unsigned>(grid), kThreads, kSmemBytes, st>>>(p);
+  dualkv_bwd_kernel<D><<<static_cast<unsigned>(grid), kThreads, L<D>::kSmemBytes, st>>>(p);
   return DKV_OK;
+}
+}  // namespace bwd
+
+int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, cudaStream_t st) {
+  if (!use_v1()) return launch_tc_bwd2(a, self, w, st);
+  return a.head_dim == 64 ? bwd::launch<64>(a, self, w, st) : bwd::launch<128>(a, self, w, st);
 }
 
 }  // namespace dkv

@@ -15,7 +15,7 @@ CASES = [
     (31, 3, 300, [77, 0, 260], 8, 2, 128, torch.bfloat16),
     (32, 2, 513, [256, 3], 4, 4, 128, torch.bfloat16),
     (33, 4, 128, [128, 1, 200, 64], 32, 8, 128, torch.bfloat16),
-    (34, 2, 200, [33, 300], 2, 2, 64, torch.bfloat16),   # d=64: tensor-core fwd, SIMT bwd
+    (34, 2, 200, [33, 300], 2, 2, 64, torch.bfloat16),   # d=64: tensor cores both ways
     (35, 4, 256, [128] * 4, 8, 8, 64, torch.float32),     # C1-like fp32: SIMT
 ]
 

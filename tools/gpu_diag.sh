@@ -1,2 +1,1 @@
-DKV_BENCH_ONE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 3 --warmup 3 > gpurun_out/b2.txt 2>&1; echo rc=$?; tail -3 gpurun_out/b2.txt | cut -c1-700
-DKV_BENCH_ONE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --impl reference --gpus 2 --steps 1 --warmup 0 > gpurun_out/b2r.txt 2>&1; echo rc=$?; tail -2 gpurun_out/b2r.txt | cut -c1-300
+for L in libdkv.so libdkv_old.so libdkv.so libdkv_old.so libdkv.so libdkv_old.so; do echo -n "$L "; DKV_LIB=$L REPS=80 timeout 200 python tools/power_probe.py bwd; done

@@ -1,5 +1,5 @@
-"""Small two-call DualKV fwd+bwd (ragged, partial tiles, R_i = 0, G = 4) and the fused repack+RoPE
-gather for compute-sanitizer."""
+"""Small two-call DualKV fwd+bwd (ragged, partial tiles, R_i = 0, G = 4), a d = 64 DualKV fwd+bwd,
+and the fused repack+RoPE gather, for compute-sanitizer."""
 import os, sys
 import numpy as np
 import torch
@@ -15,9 +15,15 @@ dec = dkv.DualKVInput(q, kc, vc, kd, vd, np.concatenate([[0], np.cumsum(rl)]))
 oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc, dec)
 for det in (True, False):
     gr = dkv.dualkv_two_call_bwd(qc, dec, oc, lc, doc, od, ld, dod, deterministic=det)
+# d = 64 (tensor-core backward with the zero-padded K^T panel)
+q64, kc64, vc64, kd64, vd64, do64 = mk(t, h, 64), mk(p, hk, 64), mk(p, hk, 64), mk(t, hk, 64), mk(t, hk, 64), mk(t, h, 64)
+in64 = dkv.DualKVInput(q64, kc64, vc64, kd64, vd64, np.concatenate([[0], np.cumsum(rl)]))
+o64, l64 = dkv.dualkv_fwd(in64)
+g64 = dkv.dualkv_bwd(in64, o64, l64, do64, deterministic=True)
 from paper_2605_15422_b200 import packing as pk  # noqa: E402
 plan = pk.make_plan([(p, rl), (31, [5, 64])])
 xs = [mk(plan.total_standard, hh, d) for hh in (h, hk, hk)]
 rq, rk, rv = dkv.repack_rope_to_dualkv(*xs, plan, 1e6)
 torch.cuda.synchronize()
-print("ok", [float(x.float().abs().sum()) for x in gr], float(rq.float().abs().sum() + rk.float().abs().sum()))
+print("ok", [float(x.float().abs().sum()) for x in gr], float(rq.float().abs().sum() + rk.float().abs().sum()),
+      [float(x.float().abs().sum()) for x in g64])
