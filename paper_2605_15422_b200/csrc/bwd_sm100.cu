@@ -15,10 +15,11 @@
 //     (kernel.py:279-285, Alg. 1/2).
 // dQ is accumulated across key tiles in fp32: each tile's dQ^T is transposed
 // through shared memory and reduce-added into dq_acc by ONE TMA bulk tensor
-// reduce (cp.reduce.async.bulk.tensor ... add) -- per-lane red.global would
-// be LSU-bound (~1 lane/clk/SM, 8K lanes per query tile).
+// reduce (cp.reduce.async.bulk.tensor ... add) -- register-sourced red.global
+// measured 2.4-4.7x slower in situ (profiles/r1_microbench.md).
 //
-// Per query tile (B_q = 64 rows, B_k = 128 keys, d = 128):
+// Per query tile (B_q = 64 rows, B_k = 128 keys, d = 128; at d = 64 the K dims of S^T / dP^T
+// and the N dims of dV / dK halve, and dQ^T keeps M = 128 over a zero-padded K^T panel):
 //   S^T  = K Q^T      (M128 N64  K128)  -> TMEM [0,64)
 //   dP^T = V dO^T     (M128 N64  K128)  -> TMEM [64,128)
 //   P^T = exp2(S^T*scale*log2e - lse2), dS^T = P^T (dP^T - D) * scale   (compute WG)
@@ -29,9 +30,10 @@
 //   dQ^T = K^T dS^T   (M128 N64  K128)  SS-MMA                  -> TMEM [192,256)
 // Roles: warps 0-7 compute (thread = key row; two warps per TMEM lane quadrant,
 // 32 query columns each, so TMEM-load latency and MUFU work of one overlap the
-// other's; part of the exponentials on the FMA pipe), 8-11 dQ drain (thread =
-// head-dim lane), 12 TMA producer + TMEM allocator, 13 MMA issuer; warps 0-7
-// run the dK / dV epilogue.
+// other's), 8-11 dQ drain (thread = head-dim lane), 12 TMA producer + TMEM
+// allocator, 13 MMA issuer; warps 0-7 run the dK / dV epilogue.  At C3 the
+// kernel runs at the board's 1000 W limit (profiles/r1_microbench.md): what
+// moves it is energy per FLOP (L2 bytes), not latency hiding.
 #include "dkv_internal.h"
 #include "tma_host.h"
 #include "trace.cuh"
