@@ -394,7 +394,33 @@ def main():
             del qx, kx, vx
         except Exception as exc:  # library missing / unsupported on this build
             ext = {"unavailable": str(exc)[:120]}
-        rep = {"ms_per_group": round(rep_ms, 3), "library_baseline": ext,
+        # and through torch's own varlen attention (torch.nn.attention.varlen.varlen_attn, causal
+        # window (-1, 0); K/V expanded to the H query heads -- it takes one head count)
+        tv = None
+        try:
+            if qr.numel() >= 2 ** 31:
+                raise RuntimeError("skipped past 2^31 query elements")
+            from torch.nn.attention.varlen import varlen_attn
+            cu_t = torch.as_tensor(s_cu, dtype=torch.int32, device=dev)
+            mx = int(np.diff(s_cu).max())
+            gq = h // hk
+            qx = qr.detach().clone().requires_grad_()
+            kx = kr.repeat_interleave(gq, dim=1).detach().requires_grad_()
+            vx = vr.repeat_interleave(gq, dim=1).detach().requires_grad_()
+
+            def tv_step():
+                o = varlen_attn(qx, kx, vx, cu_t, cu_t, mx, mx, window_size=(-1, 0))
+                o.backward(dor)
+
+            tv_step()
+            tv_ms = timed(tv_step, max(1, min(args.steps, 3)))
+            tv = {"impl": "torch.nn.attention.varlen.varlen_attn (torch " + torch.__version__ + ")",
+                  "ms_per_group": round(tv_ms, 3),
+                  "speedup_dualkv_vs_torch_varlen_ncopy": round(tv_ms / (ms / max(1, len(my_r))), 3)}
+            del qx, kx, vx
+        except Exception as exc:
+            tv = {"unavailable": str(exc)[:120]}
+        rep = {"ms_per_group": round(rep_ms, 3), "library_baseline": ext, "torch_varlen_baseline": tv,
                "tflops_algorithmic": round(14 * visible_pairs(p, rl0, "standard") * h * d / (rep_ms * 1e-3) / 1e12, 2),
                "dualkv_ms_per_group": round(grp_ms, 3),
                "speedup_dualkv_vs_ncopy": round(rep_ms / grp_ms, 3),
