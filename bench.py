@@ -122,6 +122,21 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+def cpu_host():
+    """The host the CPU arm ran on (state the CPU model, cpu_count, OPENBLAS threads)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count(),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
+
+
 def sample_desc():
     c = CPU_SAMPLE
     return (f"oracle port (numpy/OpenBLAS f32, the reference tile algorithm) fwd+bwd of Call1+Call2 at "
@@ -141,7 +156,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "C3 head shapes (H=32, Hk=8, d=128), bounded token sample", **CPU_SAMPLE},
         "cpu_baseline": {"value": round(tflops, 6), "unit": "TFLOP/s", "cores": cpu_threads(),
-                         "kind": "port", "sample": sample_desc()},
+                         "kind": "port", "sample": sample_desc(), "host": cpu_host()},
         "e2e": {"value": round(tflops, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -588,7 +603,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         tf, sec = cpu_sample_tflops(reps=1, warmup=0)
-        cpu = {"value": round(tf, 6), "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
+        cpu = {"value": round(tf, 6), "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port", "host": cpu_host(),
                "sample": sample_desc(), "seconds": round(sec, 2)}
 
     if rank == 0:
