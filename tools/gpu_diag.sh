@@ -1,1 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_rescale.py -q -p no:cacheprovider 2>&1 | tail -8
+timeout 60 ./tools/ubench/ex2_rate
