@@ -38,7 +38,10 @@
 extern "C" {
 #endif
 
-#define DKV_ABI_VERSION 1
+#define DKV_ABI_VERSION 2
+
+/* Most prompt groups one launch takes (group table entries, see dkv_group_table). */
+#define DKV_MAX_GROUPS 256
 
 #if defined(__GNUC__)
 #define DKV_API __attribute__((visibility("default")))
@@ -56,6 +59,23 @@ enum dkv_status {
 
 enum dkv_dtype { DKV_BF16 = 0, DKV_F32 = 1 };
 
+/* Multi-group launches (SURVEY §8b "group table"): several prompt groups in ONE launch.  The
+ * reference runs one group per call and loops over groups in the caller (layer.py:239,
+ * SPEC.md:284); here every group's prompt rows are concatenated in k_ctx / v_ctx (and q_ctx of
+ * the two-call op) and every group's responses in q / k / v, and the table says which rows
+ * belong together.  HOST arrays of num_groups + 1 int32 (copied into the kernel parameters):
+ *   seq_cu[g] .. seq_cu[g+1]  the sequences (indices into cu_seqlens) of group g;
+ *                             seq_cu[0] = 0, seq_cu[num_groups] = num_seqs, each group >= 1 sequence
+ *   ctx_cu[g] .. ctx_cu[g+1]  group g's prompt rows in k_ctx / v_ctx (q_ctx, out_ctx, dq_ctx);
+ *                             ctx_cu[0] = 0, ctx_cu[num_groups] = ctx_len
+ * num_groups = 0 means one group (every sequence shares rows [0, ctx_len) of the prompt).
+ * Multi-group launches run on the tensor-core path only (bf16, head_dim 64 / 128). */
+typedef struct dkv_group_table {
+  int64_t num_groups;
+  const int32_t* seq_cu;
+  const int32_t* ctx_cu;
+} dkv_group_table;
+
 typedef struct dkv_fwd_params {
   const void* q;
   const void* k_ctx; /* may be NULL when ctx_len == 0 */
@@ -69,6 +89,7 @@ typedef struct dkv_fwd_params {
   int64_t max_seqlen; /* max_i R_i (bounds the launch grid; must be >= the true max) */
   float softmax_scale;
   int32_t dtype;      /* enum dkv_dtype */
+  dkv_group_table groups; /* ABI 2: zero-initialised = one group */
 } dkv_fwd_params;
 
 typedef struct dkv_bwd_params {
@@ -93,6 +114,10 @@ typedef struct dkv_bwd_params {
   int32_t ctx_chunk;     /* sequences per context work unit; 0 = automatic */
   float* ctx_partials;   /* optional [num_chunks, 2, ctx_len, kv_heads, head_dim] f32 output of the
                             un-folded per-chunk context contributions (instrumentation hook) */
+  dkv_group_table groups; /* ABI 2: zero-initialised = one group */
+  float* ctx_grad_f32;    /* ABI 2, optional [2, ctx_len, kv_heads, head_dim] f32: the folded prompt
+                            gradient (dK_c, dV_c) just before its single cast (instrumentation:
+                            the atomic-vs-ordered fold check, SURVEY §8c "determinism") */
 } dkv_bwd_params;
 
 DKV_API int32_t dkv_abi_version(void);

@@ -24,6 +24,7 @@ from .api import (  # noqa: F401
 )
 from .costmodel import attention_flops, visible_pairs  # noqa: F401
 from .rope import RoPE, repack_rope_to_dualkv, rope_logical  # noqa: F401
-from .layer import DualKVSelfAttention  # noqa: F401
+from .layer import DualKVBatch, DualKVSelfAttention  # noqa: F401
+from . import library  # noqa: F401  (torch.library ops: dualkv::fwd/bwd/two_call_fwd/two_call_bwd/rope)
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"

@@ -21,6 +21,15 @@ _i64 = ctypes.c_int64
 _vp = ctypes.c_void_p
 
 
+DKV_ABI_VERSION = 2
+DKV_MAX_GROUPS = 256
+
+
+class GroupTable(ctypes.Structure):
+    """dkv_group_table: HOST int32 arrays of num_groups + 1 (0 groups = one group)."""
+    _fields_ = [("num_groups", _i64), ("seq_cu", _vp), ("ctx_cu", _vp)]
+
+
 class FwdParams(ctypes.Structure):
     _fields_ = [
         ("q", _vp), ("k_ctx", _vp), ("v_ctx", _vp), ("k", _vp), ("v", _vp),
@@ -28,6 +37,7 @@ class FwdParams(ctypes.Structure):
         ("num_seqs", _i64), ("total_q", _i64), ("ctx_len", _i64), ("heads", _i64),
         ("kv_heads", _i64), ("head_dim", _i64), ("max_seqlen", _i64),
         ("softmax_scale", ctypes.c_float), ("dtype", ctypes.c_int32),
+        ("groups", GroupTable),
     ]
 
 
@@ -40,7 +50,7 @@ class BwdParams(ctypes.Structure):
         ("kv_heads", _i64), ("head_dim", _i64), ("max_seqlen", _i64),
         ("softmax_scale", ctypes.c_float), ("dtype", ctypes.c_int32),
         ("deterministic", ctypes.c_int32), ("ctx_chunk", ctypes.c_int32),
-        ("ctx_partials", _vp),
+        ("ctx_partials", _vp), ("groups", GroupTable), ("ctx_grad_f32", _vp),
     ]
 
 
@@ -93,7 +103,7 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.dkv_abi_version() != 1:
+    if lib.dkv_abi_version() != DKV_ABI_VERSION:
         raise ImportError("libdkv.so ABI version mismatch")
     return lib
 

@@ -3,8 +3,8 @@
 Mirrors `/root/reference/pkg/src/dualkv/{kernel,fa2}.py` -- same names,
 argument order and meaning, and the same ValueError conditions -- but takes
 CUDA `torch.Tensor`s (bf16 or fp32) and runs every computation through the
-C ABI of libdkv.so on the caller's current CUDA stream.  PyTorch provides
-device memory, streams and autograd plumbing only.
+C ABI of libdkv.so on the current CUDA stream of the tensors' device.
+PyTorch provides device memory, streams and autograd plumbing only.
 
 Differences from the CPU reference, by design:
   * the saved forward output O is returned in the storage dtype (bf16 for
@@ -12,12 +12,22 @@ Differences from the CPU reference, by design:
   * `tile_size` is accepted and ignored (results are tile-independent,
     verify.py:297-322); the GPU tiles are 128 x 128;
   * `fold_seed` is accepted; with ``deterministic=False`` the shared-prompt
-    fold order is whatever order the hardware atomics complete in.
+    fold order is whatever order the hardware atomics complete in;
+  * `cu_seqlens` may be a CUDA int32/int64 tensor: given together with the
+    max sequence length it is used as is, with no host synchronisation (the
+    values are the caller's contract, as in flash-attn's varlen API);
+    otherwise it is copied to the host once and validated like the reference;
+  * several prompt groups can run in ONE launch (`group_seq_cu` /
+    `group_ctx_cu`, the C ABI's group table): the reference loops over groups
+    in its caller (layer.py:239).
 """
 
 from __future__ import annotations
 
+import copy
+import ctypes
 import math
+import threading
 from dataclasses import dataclass
 from typing import List, Optional, Sequence, Tuple
 
@@ -41,15 +51,17 @@ def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
     return None if t is None or t.numel() == 0 else t.data_ptr()
 
 
-def _stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
+def _stream(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
 
 
-def _check_tensor(t, name, ndim=3):
+def _check_tensor(t, name, ndim=3, device=None):
     if not isinstance(t, torch.Tensor):
         raise ValueError(f"{name} must be a torch.Tensor")
     if not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor (the op has no CPU path)")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, the other inputs on {device}")
     if t.dim() != ndim:
         raise ValueError(f"{name} must be {ndim}-D, got shape {tuple(t.shape)}")
     if t.dtype not in _DTYPES:
@@ -57,40 +69,85 @@ def _check_tensor(t, name, ndim=3):
     return t.contiguous()
 
 
-def _offsets(cu, total: int, what: str) -> Tuple[np.ndarray, torch.Tensor]:
-    """Host copy (validated as kernel.py:79-82 / fa2.py:72-75) + device int32 copy."""
-    if isinstance(cu, torch.Tensor):
-        dev = cu if cu.is_cuda else None
-        host = cu.detach().to("cpu", torch.int64).numpy()
-    else:
-        dev = None
-        host = np.asarray(cu, dtype=np.int64)
+def _validate_offsets(host: np.ndarray, total: int, what: str) -> None:
+    """kernel.py:79-82 / fa2.py:72-75."""
     if host.ndim != 1 or host.size < 2 or host[0] != 0 or host[-1] != total:
         raise ValueError(f"malformed {what} {host!r} for T={total}")
     if np.any(np.diff(host) < 0):
         raise ValueError(f"{what} must be non-decreasing")
-    if dev is None or dev.dtype != torch.int32:
-        dev = _device_offsets(host)
-    return host, dev.contiguous()
+
+
+def _offsets(cu, total: int, what: str, device: torch.device, max_len: Optional[int]):
+    """-> (host int64 copy or None, device int32 tensor, number of sequences, true max or None).
+
+    A CUDA tensor with `max_len` given is trusted and never read on the host (no device sync);
+    everything else is validated on the host first."""
+    if isinstance(cu, torch.Tensor) and cu.is_cuda:
+        if cu.device != device:
+            raise ValueError(f"{what} is on {cu.device}, the tensors on {device}")
+        if cu.dim() != 1 or cu.numel() < 2:
+            raise ValueError(f"malformed {what}: shape {tuple(cu.shape)}")
+        dev = (cu if cu.dtype == torch.int32 else cu.to(torch.int32)).contiguous()
+        if max_len is not None:
+            return None, dev, cu.numel() - 1, None
+        host = cu.detach().to("cpu", torch.int64).numpy()
+    else:
+        host = np.asarray(cu.detach().cpu().numpy() if isinstance(cu, torch.Tensor) else cu, dtype=np.int64)
+        dev = None
+    _validate_offsets(host, total, what)
+    if dev is None:
+        dev = _device_offsets(host, device)
+    lens = np.diff(host)
+    return host, dev, host.size - 1, int(lens.max()) if lens.size else 0
 
 
 _CU_CACHE: dict = {}
+_CU_LOCK = threading.Lock()
 
 
-def _device_offsets(host: np.ndarray) -> torch.Tensor:
-    """int32 device copy of host offsets, cached by content: the first use pays one synchronous
-    copy, every later call with the same offsets (every training step of a fixed layout) enqueues
-    nothing -- a per-call pageable copy would block the host on the current stream."""
-    key = (torch.cuda.current_device(), host.tobytes())
-    dev = _CU_CACHE.get(key)
-    if dev is None:
-        if len(_CU_CACHE) >= 256:  # rare: drop the cache once no kernel can still read it
-            for d in {k[0] for k in _CU_CACHE}:
-                torch.cuda.synchronize(d)
-            _CU_CACHE.clear()
-        dev = torch.as_tensor(host.astype(np.int32), device="cuda")
-        _CU_CACHE[key] = dev
+def _device_offsets(host: np.ndarray, device: torch.device) -> torch.Tensor:
+    """int32 device copy of host offsets, cached by (device, content): the first use pays one
+    synchronous copy, every later call with the same offsets (every training step of a fixed
+    layout) enqueues nothing -- a per-call pageable copy would block the host."""
+    key = (device.index, host.tobytes())
+    with _CU_LOCK:
+        dev = _CU_CACHE.get(key)
+        if dev is None:
+            if len(_CU_CACHE) >= 256:  # rare: drop the cache once no kernel can still read it
+                for d in {k[0] for k in _CU_CACHE}:
+                    torch.cuda.synchronize(d)
+                _CU_CACHE.clear()
+            dev = torch.as_tensor(host.astype(np.int32), device=device)
+            _CU_CACHE[key] = dev
     return dev
+
+
+def _group_table(seq_cu, ctx_cu, n_seqs: int, p_total: int):
+    """Validated host int32 copies of a multi-group table (include/dkv.h dkv_group_table), or None."""
+    if seq_cu is None and ctx_cu is None:
+        return None
+    if seq_cu is None or ctx_cu is None:
+        raise ValueError("group_seq_cu and group_ctx_cu go together")
+    s = np.asarray(seq_cu, dtype=np.int64)
+    c = np.asarray(ctx_cu, dtype=np.int64)
+    if s.ndim != 1 or c.shape != s.shape or s.size < 2:
+        raise ValueError("group tables must be 1-D of equal length >= 2")
+    if s.size - 1 > _lib.DKV_MAX_GROUPS:
+        raise ValueError(f"at most {_lib.DKV_MAX_GROUPS} groups per launch")
+    if s[0] != 0 or s[-1] != n_seqs or np.any(np.diff(s) <= 0):
+        raise ValueError(f"group_seq_cu {s!r} must rise strictly from 0 to N={n_seqs} "
+                         "(every group has at least one sequence)")
+    if c[0] != 0 or c[-1] != p_total or np.any(np.diff(c) < 0):
+        raise ValueError(f"group_ctx_cu {c!r} must rise from 0 to the prompt rows {p_total}")
+    return np.ascontiguousarray(s, dtype=np.int32), np.ascontiguousarray(c, dtype=np.int32)
+
+
+def _set_groups(dst, table) -> None:
+    if table is None:
+        dst.num_groups, dst.seq_cu, dst.ctx_cu = 0, None, None
+    else:
+        dst.num_groups = table[0].size - 1
+        dst.seq_cu, dst.ctx_cu = table[0].ctypes.data, table[1].ctypes.data
 
 
 def uses_tensor_cores(dtype: torch.dtype, head_dim: int, heads: int, kv_heads: int) -> bool:
@@ -103,7 +160,11 @@ def uses_tensor_cores(dtype: torch.dtype, head_dim: int, heads: int, kv_heads: i
 
 @dataclass
 class DualKVInput:
-    """Five-tensor contract of the two-region kernel (kernel.py:52-114)."""
+    """Five-tensor contract of the two-region kernel (kernel.py:52-114).
+
+    Extension: `group_seq_cu` / `group_ctx_cu` (host, N_groups + 1) put several prompt groups in
+    one launch -- k_context / v_context then hold every group's prompt rows back to back and
+    `context_seqlen` is their total."""
 
     q: torch.Tensor          # [sum R_i, H, d]
     k_context: torch.Tensor  # [P, H_k, d]
@@ -116,15 +177,19 @@ class DualKVInput:
     softmax_scale: Optional[float] = None
     causal: bool = True
     tile_size: int = 64
+    group_seq_cu: Optional[Sequence[int]] = None
+    group_ctx_cu: Optional[Sequence[int]] = None
 
     def __post_init__(self):
         self.q = _check_tensor(self.q, "q")
+        dev = self.q.device
         t_dec, h, d = self.q.shape
-        self.cu_host, self.cu_dev = _offsets(self.cu_seqlens_q, t_dec, "cu_seqlens_q")
-        self.k_context = _check_tensor(self.k_context, "k_context")
-        self.v_context = _check_tensor(self.v_context, "v_context")
-        self.k_decoded = _check_tensor(self.k_decoded, "k_decoded")
-        self.v_decoded = _check_tensor(self.v_decoded, "v_decoded")
+        self.cu_host, self.cu_dev, self._n, true_max = _offsets(self.cu_seqlens_q, t_dec, "cu_seqlens_q", dev,
+                                                               self.max_seqlen_q)
+        self.k_context = _check_tensor(self.k_context, "k_context", device=dev)
+        self.v_context = _check_tensor(self.v_context, "v_context", device=dev)
+        self.k_decoded = _check_tensor(self.k_decoded, "k_decoded", device=dev)
+        self.v_decoded = _check_tensor(self.v_decoded, "v_decoded", device=dev)
         if self.k_context.shape != self.v_context.shape:
             raise ValueError("k_context / v_context shape mismatch")
         if self.k_decoded.shape != self.v_decoded.shape:
@@ -152,15 +217,28 @@ class DualKVInput:
             raise ValueError(f"all five tensors must share one dtype, got {dts}")
         if self.softmax_scale is None:
             self.softmax_scale = 1.0 / math.sqrt(d)
-        lens = np.diff(self.cu_host)
-        true_max = int(lens.max()) if lens.size else 0
         if self.max_seqlen_q is None:
             self.max_seqlen_q = true_max
-        self._grid_max = max(int(self.max_seqlen_q), true_max)
+        if self.max_seqlen_q < 0:
+            raise ValueError("max_seqlen_q must be non-negative")
+        self._grid_max = max(int(self.max_seqlen_q), true_max or 0)
+        self._groups = _group_table(self.group_seq_cu, self.group_ctx_cu, self._n, self.context_seqlen)
 
     @property
     def num_sequences(self) -> int:
-        return self.cu_host.size - 1
+        return self._n
+
+    @property
+    def num_groups(self) -> int:
+        return 1 if self._groups is None else self._groups[0].size - 1
+
+    def _rebind(self, q, k_context, v_context, k_decoded, v_decoded) -> "DualKVInput":
+        """The same (validated) metadata over other tensors of identical shapes (autograd saves
+        the tensors through save_for_backward and rebuilds the input in backward)."""
+        new = copy.copy(self)
+        new.q, new.k_context, new.v_context, new.k_decoded, new.v_decoded = (
+            q, k_context, v_context, k_decoded, v_decoded)
+        return new
 
 
 @dataclass
@@ -177,10 +255,12 @@ class VarlenBatch:
 
     def __post_init__(self):
         self.q = _check_tensor(self.q, "q")
+        dev = self.q.device
         t_total, h, d = self.q.shape
-        self.cu_host, self.cu_dev = _offsets(self.cu_seqlens, t_total, "cu_seqlens")
-        self.k = _check_tensor(self.k, "k")
-        self.v = _check_tensor(self.v, "v")
+        self.cu_host, self.cu_dev, self._n, true_max = _offsets(self.cu_seqlens, t_total, "cu_seqlens", dev,
+                                                               self.max_seqlen)
+        self.k = _check_tensor(self.k, "k", device=dev)
+        self.v = _check_tensor(self.v, "v", device=dev)
         if self.k.shape != self.v.shape or self.k.shape[0] != t_total or self.k.shape[2] != d:
             raise ValueError(f"K/V shape {tuple(self.k.shape)} inconsistent with Q {tuple(self.q.shape)}")
         h_k = self.k.shape[1]
@@ -192,22 +272,20 @@ class VarlenBatch:
             raise ValueError("q/k/v must share one dtype")
         if self.softmax_scale is None:
             self.softmax_scale = 1.0 / math.sqrt(d)
-        lens = np.diff(self.cu_host)
-        true_max = int(lens.max()) if lens.size else 0
         if self.max_seqlen is None:
             self.max_seqlen = true_max
-        self._grid_max = max(int(self.max_seqlen), true_max)
+        self._grid_max = max(int(self.max_seqlen), true_max or 0)
 
     @property
     def num_sequences(self) -> int:
-        return self.cu_host.size - 1
+        return self._n
 
 
 # ---------------------------------------------------------------------------
 # forward (kernel.py:177-210, fa2.py:237-265)
 # ---------------------------------------------------------------------------
 
-def _fwd_params(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse):
+def _fwd_params(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse, groups=None):
     t, h, d = q.shape
     prm = FwdParams()
     prm.q, prm.k_ctx, prm.v_ctx, prm.k, prm.v = _ptr(q), _ptr(kc), _ptr(vc), _ptr(k), _ptr(v)
@@ -217,34 +295,33 @@ def _fwd_params(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse):
     prm.max_seqlen = grid_max
     prm.softmax_scale = float(scale)
     prm.dtype = _DTYPES[q.dtype]
+    _set_groups(prm.groups, groups)
     return prm
 
 
 def dualkv_fwd(inp: DualKVInput) -> Tuple[torch.Tensor, torch.Tensor]:
     """Two-region forward -> (O [sum R_i, H, d], lse [H, sum R_i] f32)."""
     q = inp.q
-    out = torch.empty_like(q)
-    lse = torch.empty((q.shape[1], q.shape[0]), dtype=torch.float32, device=q.device)
-    prm = _fwd_params(q, inp.k_context, inp.v_context, inp.k_decoded, inp.v_decoded, inp.cu_dev,
-                      inp.num_sequences, inp.context_seqlen, inp._grid_max, inp.softmax_scale, out, lse)
-    check(lib.dkv_dualkv_fwd(ctypes_ref(prm), _stream()), "dualkv_fwd")
+    with torch.cuda.device(q.device):
+        out = torch.empty_like(q)
+        lse = torch.empty((q.shape[1], q.shape[0]), dtype=torch.float32, device=q.device)
+        prm = _fwd_params(q, inp.k_context, inp.v_context, inp.k_decoded, inp.v_decoded, inp.cu_dev,
+                          inp.num_sequences, inp.context_seqlen, inp._grid_max, inp.softmax_scale, out, lse,
+                          inp._groups)
+        check(lib.dkv_dualkv_fwd(ctypes.byref(prm), _stream(q.device)), "dualkv_fwd")
     return out, lse
 
 
 def fa2_varlen_fwd(batch: VarlenBatch) -> Tuple[torch.Tensor, torch.Tensor]:
     """Per-sequence causal attention -> (O [T, H, d], lse [H, T] f32)."""
     q = batch.q
-    out = torch.empty_like(q)
-    lse = torch.empty((q.shape[1], q.shape[0]), dtype=torch.float32, device=q.device)
-    prm = _fwd_params(q, None, None, batch.k, batch.v, batch.cu_dev, batch.num_sequences, 0,
-                      batch._grid_max, batch.softmax_scale, out, lse)
-    check(lib.dkv_varlen_fwd(ctypes_ref(prm), _stream()), "fa2_varlen_fwd")
+    with torch.cuda.device(q.device):
+        out = torch.empty_like(q)
+        lse = torch.empty((q.shape[1], q.shape[0]), dtype=torch.float32, device=q.device)
+        prm = _fwd_params(q, None, None, batch.k, batch.v, batch.cu_dev, batch.num_sequences, 0,
+                          batch._grid_max, batch.softmax_scale, out, lse)
+        check(lib.dkv_varlen_fwd(ctypes.byref(prm), _stream(q.device)), "fa2_varlen_fwd")
     return out, lse
-
-
-def ctypes_ref(s):
-    import ctypes
-    return ctypes.byref(s)
 
 
 # ---------------------------------------------------------------------------
@@ -252,9 +329,12 @@ def ctypes_ref(s):
 # ---------------------------------------------------------------------------
 
 def _bwd_params(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse, d_out, deterministic,
-                ctx_chunk=0):
-    """Shape checks, output allocation and the C parameter block of one backward."""
+                ctx_chunk=0, groups=None):
+    """Shape checks (kernel.py:214-218), output allocation and the C parameter block of one backward."""
     t, h, d = q.shape
+    for name, x in (("O", out), ("dO", d_out), ("lse", lse)):
+        if not isinstance(x, torch.Tensor) or not x.is_cuda or x.device != q.device:
+            raise ValueError(f"{name} must be a CUDA tensor on {q.device}")
     if tuple(d_out.shape) != tuple(q.shape) or tuple(out.shape) != tuple(q.shape):
         raise ValueError(f"O/dO shape {tuple(out.shape)}/{tuple(d_out.shape)} inconsistent with q "
                          f"{tuple(q.shape)}")
@@ -277,41 +357,53 @@ def _bwd_params(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse, d_
     prm.dtype = _DTYPES[q.dtype]
     prm.deterministic = 1 if deterministic else 0
     prm.ctx_chunk = int(ctx_chunk)
+    _set_groups(prm.groups, groups)
     return prm, (dq, dkc, dvc, dk, dv), keep
 
 
+def _ctx_f32(prm, kc, q) -> Optional[torch.Tensor]:
+    if kc is None or kc.shape[0] == 0:
+        return torch.zeros((2, 0) + tuple(kc.shape[1:] if kc is not None else (0, q.shape[2])),
+                           dtype=torch.float32, device=q.device)
+    buf = torch.empty((2,) + tuple(kc.shape), dtype=torch.float32, device=q.device)
+    prm.ctx_grad_f32 = buf.data_ptr()
+    return buf
+
+
 def _bwd_run(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse, d_out, deterministic,
-             ctx_chunk=0, partials_for_chunks=False, varlen=False):
-    prm, grads, keep = _bwd_params(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse, d_out,
-                                   deterministic, ctx_chunk)
-    partials = None
-    if partials_for_chunks:
-        nch = int(lib.dkv_bwd_num_ctx_chunks(ctypes_ref(prm)))
-        kk = kc if kc is not None else k
-        partials = torch.empty((nch, 2, p_len, kk.shape[1], q.shape[2]), dtype=torch.float32, device=q.device)
-        prm.ctx_partials = _ptr(partials)
-    ws_bytes = int(lib.dkv_bwd_workspace_size(ctypes_ref(prm)))
-    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)
-    fn = lib.dkv_varlen_bwd if varlen else lib.dkv_dualkv_bwd
-    check(fn(ctypes_ref(prm), ws.data_ptr(), ws_bytes, _stream()),
-          "fa2_varlen_bwd" if varlen else "dualkv_bwd")
-    del keep
-    return grads + (partials,)
+             ctx_chunk=0, partials_for_chunks=False, varlen=False, groups=None, want_f32=False):
+    with torch.cuda.device(q.device):
+        prm, grads, keep = _bwd_params(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse, d_out,
+                                       deterministic, ctx_chunk, groups)
+        partials = None
+        if partials_for_chunks:
+            nch = int(lib.dkv_bwd_num_ctx_chunks(ctypes.byref(prm)))
+            kk = kc if kc is not None else k
+            partials = torch.empty((nch, 2, p_len, kk.shape[1], q.shape[2]), dtype=torch.float32,
+                                   device=q.device)
+            prm.ctx_partials = _ptr(partials)
+        f32 = _ctx_f32(prm, kc, q) if want_f32 else None
+        ws_bytes = int(lib.dkv_bwd_workspace_size(ctypes.byref(prm)))
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)
+        fn = lib.dkv_varlen_bwd if varlen else lib.dkv_dualkv_bwd
+        check(fn(ctypes.byref(prm), ws.data_ptr(), ws_bytes, _stream(q.device)),
+              "fa2_varlen_bwd" if varlen else "dualkv_bwd")
+        del keep
+    return grads + (partials, f32)
 
 
 def dualkv_bwd(inp: DualKVInput, out, lse, d_out, deterministic: bool = True,
-               fold_seed: Optional[int] = None):
+               fold_seed: Optional[int] = None, *, return_context_f32: bool = False):
     """Two-region backward -> (dQ_d, dK_c, dV_c, dK_d, dV_d) in storage dtype.
 
-    dK_c/dV_c are the fp32 sum over all sequences cast once
-    (kernel.py:279-285).  ``fold_seed`` is accepted for interface parity.
-    """
+    dK_c/dV_c are the fp32 sum over all sequences cast once (kernel.py:279-285).
+    ``fold_seed`` is accepted for interface parity.  ``return_context_f32`` (instrumentation)
+    appends the fp32 [2, P, H_k, d] prompt gradient the cast was applied to."""
     del fold_seed
-    dq, dkc, dvc, dkd, dvd, _ = _bwd_run(
-        inp.q, inp.k_context, inp.v_context, inp.k_decoded, inp.v_decoded, inp.cu_dev,
-        inp.num_sequences, inp.context_seqlen, inp._grid_max, inp.softmax_scale, out, lse, d_out,
-        deterministic)
-    return dq, dkc, dvc, dkd, dvd
+    res = _bwd_run(inp.q, inp.k_context, inp.v_context, inp.k_decoded, inp.v_decoded, inp.cu_dev,
+                   inp.num_sequences, inp.context_seqlen, inp._grid_max, inp.softmax_scale, out, lse, d_out,
+                   deterministic, groups=inp._groups, want_f32=return_context_f32)
+    return res[:5] + ((res[6],) if return_context_f32 else ())
 
 
 def context_grad_contributions(inp: DualKVInput, out, lse, d_out) -> List[Tuple[torch.Tensor, torch.Tensor]]:
@@ -319,19 +411,22 @@ def context_grad_contributions(inp: DualKVInput, out, lse, d_out) -> List[Tuple[
 
     Zero-length sequences contribute nothing and are skipped, as in the
     reference generator (kernel.py:231-234)."""
+    if inp._groups is not None:
+        raise ValueError("context_grad_contributions takes one prompt group")
     res = _bwd_run(inp.q, inp.k_context, inp.v_context, inp.k_decoded, inp.v_decoded, inp.cu_dev,
                    inp.num_sequences, inp.context_seqlen, inp._grid_max, inp.softmax_scale, out, lse,
                    d_out, True, ctx_chunk=1, partials_for_chunks=True)
     parts = res[5]
-    lens = np.diff(inp.cu_host)
+    host = inp.cu_host if inp.cu_host is not None else inp.cu_dev.cpu().numpy()  # instrumentation: may sync
+    lens = np.diff(np.asarray(host, dtype=np.int64))
     return [(parts[i, 0], parts[i, 1]) for i in range(inp.num_sequences) if lens[i] > 0]
 
 
 def fa2_varlen_bwd(batch: VarlenBatch, out, lse, d_out):
     """Backward of `fa2_varlen_fwd` -> (dQ, dK, dV) in storage dtype (fa2.py:268-306)."""
-    dq, _, _, dk, dv, _ = _bwd_run(batch.q, None, None, batch.k, batch.v, batch.cu_dev,
-                                   batch.num_sequences, 0, batch._grid_max, batch.softmax_scale, out,
-                                   lse, d_out, True, varlen=True)
+    dq, _, _, dk, dv, _, _ = _bwd_run(batch.q, None, None, batch.k, batch.v, batch.cu_dev,
+                                      batch.num_sequences, 0, batch._grid_max, batch.softmax_scale, out,
+                                      lse, d_out, True, varlen=True)
     return dq, dk, dv
 
 
@@ -363,9 +458,10 @@ def convert_dkv_context(scratch: ContextGradScratch, out_dtype=torch.bfloat16):
     outs = []
     for acc in (scratch.dk_acc, scratch.dv_acc):
         acc = acc.to(torch.float32).contiguous()
-        dst = torch.empty(acc.shape, dtype=torch.bfloat16, device=acc.device)
-        check(lib.dkv_convert_f32_to_bf16(_ptr(acc), _ptr(dst), acc.numel(), _stream()),
-              "convert_dkv_context")
+        with torch.cuda.device(acc.device):
+            dst = torch.empty(acc.shape, dtype=torch.bfloat16, device=acc.device)
+            check(lib.dkv_convert_f32_to_bf16(_ptr(acc), _ptr(dst), acc.numel(), _stream(acc.device)),
+                  "convert_dkv_context")
         outs.append(dst)
     return outs[0], outs[1]
 
@@ -382,51 +478,11 @@ def bf16_naive_accumulate(contributions) -> torch.Tensor:
 
 
 # ---------------------------------------------------------------------------
-# five-tensor autograd surface (kernel.py:308-348)
-# ---------------------------------------------------------------------------
-
-class _DualKVFunction(torch.autograd.Function):
-    @staticmethod
-    def forward(ctx, q, k_context, v_context, k_decoded, v_decoded, inp):
-        out, lse = dualkv_fwd(inp)
-        ctx.save_for_backward(out, lse)
-        ctx.inp = inp
-        return out
-
-    @staticmethod
-    def backward(ctx, d_out):
-        out, lse = ctx.saved_tensors
-        dq, dkc, dvc, dkd, dvd = dualkv_bwd(ctx.inp, out, lse, d_out.contiguous(), deterministic=False)
-        return dq, dkc, dvc, dkd, dvd, None
-
-
-def dualkv_attention_varlen(q, k_context, v_context, k_decoded, v_decoded, cu_seqlens_q,
-                            cu_seqlens_k_decoded=None, max_seqlen_q: Optional[int] = None,
-                            context_seqlen: Optional[int] = None,
-                            max_seqlen_k_decoded: Optional[int] = None,
-                            softmax_scale: Optional[float] = None, causal: bool = True,
-                            tile_size: int = 64) -> torch.Tensor:
-    """Five-tensor call surface; lse is saved on the autograd ctx, not returned."""
-    if cu_seqlens_k_decoded is not None:
-        a = np.asarray(cu_seqlens_k_decoded.cpu() if isinstance(cu_seqlens_k_decoded, torch.Tensor)
-                       else cu_seqlens_k_decoded)
-        b = np.asarray(cu_seqlens_q.cpu() if isinstance(cu_seqlens_q, torch.Tensor) else cu_seqlens_q)
-        if not np.array_equal(a, b):
-            raise ValueError("cu_seqlens_k_decoded must equal cu_seqlens_q")
-    del max_seqlen_k_decoded  # decoded KV shares q's offsets (kernel.py:333)
-    inp = DualKVInput(q, k_context, v_context, k_decoded, v_decoded, cu_seqlens_q,
-                      context_seqlen=context_seqlen, max_seqlen_q=max_seqlen_q,
-                      softmax_scale=softmax_scale, causal=causal, tile_size=tile_size)
-    return _DualKVFunction.apply(inp.q, inp.k_context, inp.v_context, inp.k_decoded,
-                                 inp.v_decoded, inp)
-
-
-# ---------------------------------------------------------------------------
 # fused two-call op (SURVEY §8f #1; layer.py:236-290 composed in one launch)
 # ---------------------------------------------------------------------------
 
 def _check_prompt_q(q_ctx, inp: DualKVInput):
-    q_ctx = _check_tensor(q_ctx, "q_context")
+    q_ctx = _check_tensor(q_ctx, "q_context", device=inp.q.device)
     p_len = inp.context_seqlen
     if tuple(q_ctx.shape) != (p_len, inp.q.shape[1], inp.q.shape[2]) or q_ctx.dtype != inp.q.dtype:
         raise ValueError(f"q_context shape/dtype {tuple(q_ctx.shape)}/{q_ctx.dtype} inconsistent with "
@@ -438,78 +494,103 @@ def dualkv_two_call_fwd(q_context, inp: DualKVInput):
     """Call 1 (causal self-attention of the prompt's own queries) + Call 2 (DualKV) in ONE launch.
 
     Returns (O_ctx [P,H,d], lse_ctx [H,P], O_dec [sum R_i,H,d], lse_dec [H,sum R_i]) -- equal to
-    `fa2_varlen_fwd` over the prompt and `dualkv_fwd(inp)` (layer.py:243-255)."""
+    `fa2_varlen_fwd` over the prompt and `dualkv_fwd(inp)` (layer.py:243-255).  With a group
+    table, every group's prompt is its own Call 1 sequence (rows group_ctx_cu[g]..[g+1])."""
     q_ctx = _check_prompt_q(q_context, inp)
     q = inp.q
     p_len, h, d = q_ctx.shape
-    out = torch.empty_like(q)
-    lse = torch.empty((h, q.shape[0]), dtype=torch.float32, device=q.device)
-    out_c = torch.empty_like(q_ctx)
-    lse_c = torch.empty((h, p_len), dtype=torch.float32, device=q.device)
-    prm = TwoCallFwdParams()
-    prm.call2 = _fwd_params(q, inp.k_context, inp.v_context, inp.k_decoded, inp.v_decoded, inp.cu_dev,
-                            inp.num_sequences, p_len, inp._grid_max, inp.softmax_scale, out, lse)
-    prm.q_ctx, prm.out_ctx, prm.lse_ctx = _ptr(q_ctx), _ptr(out_c), _ptr(lse_c)
-    check(lib.dkv_twocall_fwd(ctypes_ref(prm), _stream()), "dualkv_two_call_fwd")
+    with torch.cuda.device(q.device):
+        out = torch.empty_like(q)
+        lse = torch.empty((h, q.shape[0]), dtype=torch.float32, device=q.device)
+        out_c = torch.empty_like(q_ctx)
+        lse_c = torch.empty((h, p_len), dtype=torch.float32, device=q.device)
+        prm = TwoCallFwdParams()
+        prm.call2 = _fwd_params(q, inp.k_context, inp.v_context, inp.k_decoded, inp.v_decoded, inp.cu_dev,
+                                inp.num_sequences, p_len, inp._grid_max, inp.softmax_scale, out, lse, inp._groups)
+        prm.q_ctx, prm.out_ctx, prm.lse_ctx = _ptr(q_ctx), _ptr(out_c), _ptr(lse_c)
+        check(lib.dkv_twocall_fwd(ctypes.byref(prm), _stream(q.device)), "dualkv_two_call_fwd")
     return out_c, lse_c, out, lse
 
 
 def dualkv_two_call_bwd(q_context, inp: DualKVInput, out_ctx, lse_ctx, d_out_ctx, out, lse, d_out,
-                        deterministic: bool = True):
+                        deterministic: bool = True, *, return_context_f32: bool = False):
     """Backward of both calls in ONE launch.  Returns (dQ_ctx, dK_c, dV_c, dQ_dec, dK_dec, dV_dec),
     dK_c / dV_c being the TOTAL prompt-key gradient (Call 1 + Call 2, layer.py:278-279) accumulated
-    in one fp32 scratch and cast once."""
+    in one fp32 scratch and cast once (``return_context_f32`` appends that fp32 [2, P, H_k, d])."""
     q_ctx = _check_prompt_q(q_context, inp)
     p_len, h, d = q_ctx.shape
+    for name, x in (("O_ctx", out_ctx), ("dO_ctx", d_out_ctx), ("lse_ctx", lse_ctx)):
+        if not isinstance(x, torch.Tensor) or not x.is_cuda or x.device != q_ctx.device:
+            raise ValueError(f"{name} must be a CUDA tensor on {q_ctx.device}")
     if tuple(out_ctx.shape) != tuple(q_ctx.shape) or tuple(d_out_ctx.shape) != tuple(q_ctx.shape):
         raise ValueError("O_ctx/dO_ctx shape inconsistent with q_context")
     if tuple(lse_ctx.shape) != (h, p_len):
         raise ValueError(f"lse_ctx shape {tuple(lse_ctx.shape)} != {(h, p_len)}")
-    prm2, grads, keep = _bwd_params(inp.q, inp.k_context, inp.v_context, inp.k_decoded, inp.v_decoded,
-                                    inp.cu_dev, inp.num_sequences, p_len, inp._grid_max, inp.softmax_scale,
-                                    out, lse, d_out, deterministic)
-    dq, dkc, dvc, dkd, dvd = grads
-    o_c = out_ctx.to(q_ctx.dtype).contiguous()
-    l_c = lse_ctx.to(torch.float32).contiguous()
-    do_c = d_out_ctx.to(q_ctx.dtype).contiguous()
-    dq_c = torch.empty_like(q_ctx)
-    prm = TwoCallBwdParams()
-    prm.call2 = prm2
-    prm.q_ctx, prm.out_ctx, prm.lse_ctx = _ptr(q_ctx), _ptr(o_c), _ptr(l_c)
-    prm.dout_ctx, prm.dq_ctx = _ptr(do_c), _ptr(dq_c)
-    ws_bytes = int(lib.dkv_twocall_bwd_workspace_size(ctypes_ref(prm)))
-    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q_ctx.device)
-    check(lib.dkv_twocall_bwd(ctypes_ref(prm), ws.data_ptr(), ws_bytes, _stream()), "dualkv_two_call_bwd")
-    del keep
-    return dq_c, dkc, dvc, dq, dkd, dvd
+    with torch.cuda.device(q_ctx.device):
+        prm2, grads, keep = _bwd_params(inp.q, inp.k_context, inp.v_context, inp.k_decoded, inp.v_decoded,
+                                        inp.cu_dev, inp.num_sequences, p_len, inp._grid_max, inp.softmax_scale,
+                                        out, lse, d_out, deterministic, groups=inp._groups)
+        dq, dkc, dvc, dkd, dvd = grads
+        f32 = _ctx_f32(prm2, inp.k_context, inp.q) if return_context_f32 else None
+        o_c = out_ctx.to(q_ctx.dtype).contiguous()
+        l_c = lse_ctx.to(torch.float32).contiguous()
+        do_c = d_out_ctx.to(q_ctx.dtype).contiguous()
+        dq_c = torch.empty_like(q_ctx)
+        prm = TwoCallBwdParams()
+        prm.call2 = prm2
+        prm.q_ctx, prm.out_ctx, prm.lse_ctx = _ptr(q_ctx), _ptr(o_c), _ptr(l_c)
+        prm.dout_ctx, prm.dq_ctx = _ptr(do_c), _ptr(dq_c)
+        ws_bytes = int(lib.dkv_twocall_bwd_workspace_size(ctypes.byref(prm)))
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q_ctx.device)
+        check(lib.dkv_twocall_bwd(ctypes.byref(prm), ws.data_ptr(), ws_bytes, _stream(q_ctx.device)),
+              "dualkv_two_call_bwd")
+        del keep
+    res = (dq_c, dkc, dvc, dq, dkd, dvd)
+    return res + ((f32,) if return_context_f32 else ())
 
 
-class _TwoCallFunction(torch.autograd.Function):
-    @staticmethod
-    def forward(ctx, q_context, k_context, v_context, q, k_decoded, v_decoded, inp):
-        o_c, l_c, o, l = dualkv_two_call_fwd(q_context, inp)
-        ctx.save_for_backward(q_context, o_c, l_c, o, l)
-        ctx.inp = inp
-        return o_c, o
+# ---------------------------------------------------------------------------
+# autograd surfaces (kernel.py:308-348, PAPER.md:1089-1105): registered torch.library custom ops
+# (library.py) so torch.compile sees opaque ops with fake implementations instead of graph breaks
+# ---------------------------------------------------------------------------
 
-    @staticmethod
-    def backward(ctx, d_oc, d_o):
-        q_c, o_c, l_c, o, l = ctx.saved_tensors
-        d_oc = torch.zeros_like(o_c) if d_oc is None else d_oc.contiguous()
-        d_o = torch.zeros_like(o) if d_o is None else d_o.contiguous()
-        dq_c, dkc, dvc, dq, dkd, dvd = dualkv_two_call_bwd(q_c, ctx.inp, o_c, l_c, d_oc, o, l, d_o,
-                                                           deterministic=False)
-        return dq_c, dkc, dvc, dq, dkd, dvd, None
+def dualkv_attention_varlen(q, k_context, v_context, k_decoded, v_decoded, cu_seqlens_q,
+                            cu_seqlens_k_decoded=None, max_seqlen_q: Optional[int] = None,
+                            context_seqlen: Optional[int] = None,
+                            max_seqlen_k_decoded: Optional[int] = None,
+                            softmax_scale: Optional[float] = None, causal: bool = True,
+                            tile_size: int = 64) -> torch.Tensor:
+    """Five-tensor call surface; lse is saved on the autograd ctx, not returned."""
+    if cu_seqlens_k_decoded is not None and cu_seqlens_k_decoded is not cu_seqlens_q:
+        if isinstance(cu_seqlens_k_decoded, torch.Tensor) and isinstance(cu_seqlens_q, torch.Tensor) \
+                and cu_seqlens_k_decoded.device == cu_seqlens_q.device:
+            same = cu_seqlens_k_decoded.shape == cu_seqlens_q.shape and \
+                bool(torch.equal(cu_seqlens_k_decoded.to(cu_seqlens_q.dtype), cu_seqlens_q))
+        else:
+            host = lambda x: np.asarray(x.detach().cpu().numpy() if isinstance(x, torch.Tensor) else x)
+            same = np.array_equal(host(cu_seqlens_k_decoded), host(cu_seqlens_q))
+        if not same:
+            raise ValueError("cu_seqlens_k_decoded must equal cu_seqlens_q")
+    del max_seqlen_k_decoded  # decoded KV shares q's offsets (kernel.py:333)
+    inp = DualKVInput(q, k_context, v_context, k_decoded, v_decoded, cu_seqlens_q,
+                      context_seqlen=context_seqlen, max_seqlen_q=max_seqlen_q,
+                      softmax_scale=softmax_scale, causal=causal, tile_size=tile_size)
+    from . import library
+    return library.attention(inp)
 
 
 def dualkv_two_call_attention(q_context, k_context, v_context, q_decoded, k_decoded, v_decoded,
                               cu_seqlens_q, max_seqlen_q: Optional[int] = None,
-                              softmax_scale: Optional[float] = None):
-    """The whole attention of one prompt group in the P+NR layout (layer.py:236-290): returns
-    (O_context [P,H,d], O_decoded [sum R_i,H,d]); autograd gives all six input gradients, the
-    prompt K/V gradient summed over both calls and all N sequences in fp32 and cast once."""
+                              softmax_scale: Optional[float] = None,
+                              group_seq_cu: Optional[Sequence[int]] = None,
+                              group_ctx_cu: Optional[Sequence[int]] = None):
+    """The whole attention of one prompt group (or, with a group table, of several) in the P+NR
+    layout (layer.py:236-290): returns (O_context [P,H,d], O_decoded [sum R_i,H,d]); autograd gives
+    all six input gradients, the prompt K/V gradient summed over both calls and all N sequences in
+    fp32 and cast once."""
     inp = DualKVInput(q_decoded, k_context, v_context, k_decoded, v_decoded, cu_seqlens_q,
-                      max_seqlen_q=max_seqlen_q, softmax_scale=softmax_scale)
+                      max_seqlen_q=max_seqlen_q, softmax_scale=softmax_scale,
+                      group_seq_cu=group_seq_cu, group_ctx_cu=group_ctx_cu)
     q_ctx = _check_prompt_q(q_context, inp)
-    return _TwoCallFunction.apply(q_ctx, inp.k_context, inp.v_context, inp.q, inp.k_decoded,
-                                  inp.v_decoded, inp)
+    from . import library
+    return library.two_call_attention(q_ctx, inp)

@@ -132,15 +132,17 @@ void launch_rowsum_do_o(const SimtArgs& a, float* drow, __nv_bfloat16* xsplit, i
     rowsum_kernel<__nv_bfloat16><<<blocks, threads, 0, st>>>(a, drow, xsplit, tpad);
 }
 
-// dk/dv[i] = cast(sum_{c < num_parts} partials[c][0/1][i]), fixed chunk order
+// dk/dv[i] = cast(sum_{c < num_parts} partials[c][0/1][i]), fixed chunk order; f32_out (optional)
+// receives the fp32 sums [2][plane] (the instrumentation view of the value that is cast once)
 __global__ void fold_convert_kernel(const float* __restrict__ parts, int num_parts, int64_t plane, void* dk,
-                                    void* dv, int dtype) {
+                                    void* dv, int dtype, float* f32_out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= 2 * plane) return;
   const int which = static_cast<int>(i / plane);
   const int64_t e = i % plane;
   float acc = 0.f;
   for (int c = 0; c < num_parts; ++c) acc += parts[(static_cast<int64_t>(c) * 2 + which) * plane + e];
+  if (f32_out) f32_out[i] = acc;
   void* dst = which == 0 ? dk : dv;
   if (dtype == DKV_F32)
     static_cast<float*>(dst)[e] = acc;
@@ -149,11 +151,11 @@ __global__ void fold_convert_kernel(const float* __restrict__ parts, int num_par
 }
 
 void launch_fold_convert(const float* partials, int num_parts, int64_t plane, void* dk, void* dv, int dtype,
-                         cudaStream_t st) {
+                         float* f32_out, cudaStream_t st) {
   if (plane == 0) return;
   const int threads = 256;
   const int64_t blocks = (2 * plane + threads - 1) / threads;
-  fold_convert_kernel<<<blocks, threads, 0, st>>>(partials, num_parts, plane, dk, dv, dtype);
+  fold_convert_kernel<<<blocks, threads, 0, st>>>(partials, num_parts, plane, dk, dv, dtype, f32_out);
 }
 
 // vectorised f32 -> {bf16, f32}; RNE via __float2bfloat16_rn (== reference bf16_round)

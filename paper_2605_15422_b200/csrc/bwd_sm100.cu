@@ -86,7 +86,6 @@ struct Params {
   CUtensorMap tm_x;     // xsplit [Hk*tpad*G rows][32] bf16: split3(-lse/scale) | split3(-D)
   // fused Call 1 (two-call launch): the prompt's own queries, their (lse, D) rows and dQ
   CUtensorMap tm_qs, tm_dos, tm_xs, tm_dqs;
-  int cu_self[2];       // {0, P}: the prompt as a one-sequence "cu_seqlens"
   int tpad_s, n_self_items, self_part;
   float* dq_acc;        // [T][H][D] f32
   __nv_bfloat16* dk;    // [T][Hk][D]
@@ -94,11 +93,13 @@ struct Params {
   float* ctx_acc;       // [parts][2][P][Hk][D]
   const int32_t* cu;
   int num_seqs, total_q, ctx_len, heads, kv_heads, group, tq, tpad;
-  int chunk, n_ctx_items, n_ctx_tiles;
+  int chunk, max_chunks, n_ctx_items, n_ctx_tiles;  // n_ctx_tiles: of the longest group prompt
   int atomic_ctx;
   int ablate;  // timing experiments only (DKV_BWD_ABLATE): 1 drain I/O, 2 compute math, 4 Q/dO loads,
                // 8 the additive-constant MMAs
   float scale, scale_log2;
+  // prompt groups; grp.ctx doubles as the Call 1 "cu_seqlens" (group g's prompt = sequence g)
+  GroupTable grp;
 };
 
 struct Bars {
@@ -164,16 +165,21 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     kind = 0;
     // key tiles fastest: the ~148 co-resident CTAs then share a few (chunk, head) Q/dO streams
     // and dQ-accumulator regions in L2 instead of 8 heads' worth
+    // (multi-group launches: then group, then chunk -- every group's chunk 0 first)
     const int per_chunk = p.n_ctx_tiles * p.kv_heads;
-    const int chunk_id = bid / per_chunk;
+    const int cg = bid / per_chunk;  // (chunk, group)
     const int rem = bid % per_chunk;
     ktile = rem % p.n_ctx_tiles;
     hk = rem / p.n_ctx_tiles;
-    s0 = chunk_id * p.chunk;
-    s1 = min(p.num_seqs, s0 + p.chunk);
+    const int g = cg % p.grp.n;
+    const int chunk_id = cg / p.grp.n;
+    kv_row0 = p.grp.ctx[g];
+    kv_len = p.grp.ctx[g + 1] - kv_row0;
+    if (ktile * kBK >= kv_len) return;  // a shorter prompt than the launch's longest
+    s0 = p.grp.seq[g] + chunk_id * p.chunk;
+    s1 = min(p.grp.seq[g + 1], s0 + p.chunk);
+    if (s0 >= s1) return;  // a group with fewer sequences than the largest
     tok_first = 0;
-    kv_len = p.ctx_len;
-    kv_row0 = 0;
     part = p.atomic_ctx ? 0 : chunk_id;
   } else if (bid >= p.n_ctx_items + p.n_self_items) {
     kind = 1;
@@ -191,17 +197,18 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     kind = 2;
     const int b3 = bid - p.n_ctx_items;
     ktile = b3 % p.n_ctx_tiles;
-    hk = b3 / p.n_ctx_tiles;
-    s0 = 0;
-    s1 = 1;
-    kv_len = p.ctx_len;
+    hk = (b3 / p.n_ctx_tiles) % p.kv_heads;
+    s0 = b3 / (p.n_ctx_tiles * p.kv_heads);  // the group = its prompt's "sequence" in grp.ctx
+    s1 = s0 + 1;
+    kv_row0 = p.grp.ctx[s0];
+    kv_len = p.grp.ctx[s0 + 1] - kv_row0;
+    if (ktile * kBK >= kv_len) return;
     tok_first = (ktile * kBK / p.tq) * p.tq;
-    kv_row0 = 0;
     part = p.atomic_ctx ? 0 : p.self_part;
   }
   const bool ctx_keys = kind != 1;  // keys are the shared prompt copy (output -> fp32 scratch)
   const bool causal = kind != 0;
-  const int32_t* cu = kind == 2 ? p.cu_self : p.cu;
+  const int32_t* cu = kind == 2 ? p.grp.ctx : p.cu;
   const CUtensorMap* mq = kind == 2 ? &p.tm_qs : &p.tm_q;
   const CUtensorMap* mdo = kind == 2 ? &p.tm_dos : &p.tm_do;
   const CUtensorMap* mx = kind == 2 ? &p.tm_xs : &p.tm_x;
@@ -282,8 +289,8 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         mbar_wait(&bar.q_empty[st], ph ^ 1);
         TRACE(T_Q_LOAD, i);
         const int row0 = cu[it.s] + it.tok;
-        mbar_arrive_expect_tx(&bar.q_full[st], ((p.ablate & 4) ? 0 : 2 * kQBytes) + 2 * kXBytes);
-        for (int pn = 0; pn < D / 64 && !(p.ablate & 4); ++pn) {
+        mbar_arrive_expect_tx(&bar.q_full[st], ((DKV_ABL(p.ablate) & 4) ? 0 : 2 * kQBytes) + 2 * kXBytes);
+        for (int pn = 0; pn < D / 64 && !(DKV_ABL(p.ablate) & 4); ++pn) {
           tma_load_3d(base + kOffQ + st * kQBytes + pn * kQPanel, mq, &bar.q_full[st], pn * 64, hk * G, row0);
           tma_load_3d(base + kOffDO + st * kQBytes + pn * kQPanel, mdo, &bar.q_full[st], pn * 64, hk * G, row0);
         }
@@ -328,11 +335,11 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) mma_ss(tS, dKk + koff_kv(k), dQk + koff_q(k), id_sdp, k > 0);
           // S^T[k][c] += -lse[c] / scale  (so that P = exp2(S'^T * scale * log2 e))
-          if (!(p.ablate & 8)) mma_ss(tS, dOnes, dX, id_sdp, 1u);
+          if (!(DKV_ABL(p.ablate) & 8)) mma_ss(tS, dOnes, dX, id_sdp, 1u);
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) mma_ss(tdP, dVk + koff_kv(k), dOk + koff_q(k), id_sdp, k > 0);
           // dP^T[k][c] += -D[c]  (so that dS^T = P^T * dP'^T)
-          if (!(p.ablate & 8)) mma_ss(tdP, dOnes, dX + (kXBytes >> 4), id_sdp, 1u);
+          if (!(DKV_ABL(p.ablate) & 8)) mma_ss(tdP, dOnes, dX + (kXBytes >> 4), id_sdp, 1u);
           mma_commit(&bar.sdp_full);
         }
         if (i > 0) {
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       uint32_t pp[16], pd[16];
       // S' = S - lse/scale and dP' = dP - D arrive from the MMA: P = exp2(S' scale log2e),
       // dS = P dP' (the softmax scale is applied once to dK in the epilogue and dQ in its cast)
-      if (p.ablate & 2) {
+      if (DKV_ABL(p.ablate) & 2) {
 #pragma unroll
         for (int c2 = 0; c2 < 16; ++c2) {
           pp[c2] = us[2 * c2] ^ us[2 * c2 + 1];
@@ -476,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       // transpose through smem ([row][d] fp32) and reduce-add into dq_acc with TMA bulk tensor
       // reduces, one per 32-row half: reductions leave an SM at ~25 B/clk (profiles/
       // r1_microbench.md), so the staging of one half overlaps the other half's egress
-      if (p.ablate & 1) continue;
+      if (DKV_ABL(p.ablate) & 1) continue;
       const int row0 = cu[it.s] + it.tok;
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
@@ -521,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       if (ctx_keys) {
         const int64_t plane = static_cast<int64_t>(p.ctx_len) * p.kv_heads * D;
         float* dst = p.ctx_acc + static_cast<int64_t>(part) * 2 * plane +
-                     (do_k ? 0 : plane) + (static_cast<int64_t>(key) * p.kv_heads + hk) * D + c0;
+                     (do_k ? 0 : plane) + ((static_cast<int64_t>(kv_row0) + key) * p.kv_heads + hk) * D + c0;
         if (p.atomic_ctx) {
 #pragma unroll
           for (int i = 0; i < 32; i += 4)
@@ -556,16 +563,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
 
 DKV_TRACE_READ_FN(dkv_trace_read_v1)
 
-// DKV_BWD_V2=1: bwd2_sm100.cu's 128x128-tile kernel instead of the 64-row one below (experimental:
-// same speed today, and its dS uses the bf16-rounded P -- see DESIGN.md §4.2c)
-static bool use_v1() {
-  static const bool v = [] {
-    const char* e = getenv("DKV_BWD_V2");
-    return !(e && e[0] == '1');
-  }();
-  return v;
-}
-
 static bool tc_bwd1_supported(int head_dim, int heads, int kv_heads) {
   if ((head_dim != 64 && head_dim != 128) || kv_heads <= 0 || heads % kv_heads) return false;
   const int G = heads / kv_heads;
@@ -574,12 +571,13 @@ static bool tc_bwd1_supported(int head_dim, int heads, int kv_heads) {
 
 bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads) {
   if (dtype != DKV_BF16 || force_simt()) return false;
-  return use_v1() ? tc_bwd1_supported(head_dim, heads, kv_heads) : tc_bwd2_supported(head_dim, heads, kv_heads);
+  return tc_bwd1_supported(head_dim, heads, kv_heads);
 }
 
 namespace bwd {
 template <int D>
-static int launch(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, cudaStream_t st) {
+static int launch(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, const BwdScratch& w,
+                  cudaStream_t st) {
   Params p{};
   const int G = a.heads / a.kv_heads;
   const int tq = kBQ / G;
@@ -612,8 +610,7 @@ static int launch(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, c
   }
   p.tpad = w.tpad;
   p.tpad_s = w.tpad_s;
-  p.cu_self[0] = 0;
-  p.cu_self[1] = a.ctx_len;
+  p.grp = grp;
   p.dq_acc = w.dq_acc;
   p.dk = static_cast<__nv_bfloat16*>(a.dk);
   p.dv = static_cast<__nv_bfloat16*>(a.dv);
@@ -627,15 +624,25 @@ static int launch(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, c
   p.group = G;
   p.tq = tq;
   p.chunk = w.chunk;
-  p.n_ctx_tiles = (a.ctx_len + kBK - 1) / kBK;
-  p.n_ctx_items = a.total_q > 0 ? p.n_ctx_tiles * a.kv_heads * w.num_chunks : 0;
-  p.n_self_items = with_self ? p.n_ctx_tiles * a.kv_heads : 0;
+  p.max_chunks = w.num_chunks;
+  p.n_ctx_tiles = (grp.max_ctx + kBK - 1) / kBK;
+  const int64_t n_ctx_items =
+      a.total_q > 0 ? static_cast<int64_t>(p.n_ctx_tiles) * a.kv_heads * grp.n * w.num_chunks : 0;
+  const int64_t n_self_items = with_self ? static_cast<int64_t>(p.n_ctx_tiles) * a.kv_heads * grp.n : 0;
+  if (n_ctx_items + n_self_items > 0x7fffffff) {
+    set_error("backward grid too large");
+    return DKV_ERR_UNSUPPORTED;
+  }
+  p.n_ctx_items = static_cast<int>(n_ctx_items);
+  p.n_self_items = static_cast<int>(n_self_items);
   p.self_part = w.self_part;
   p.atomic_ctx = w.atomic_ctx ? 1 : 0;
+#ifdef DKV_ABLATION  // timing-experiment builds only (libdkv_trace.so); never read by libdkv.so
   {
     const char* e = getenv("DKV_BWD_ABLATE");
     p.ablate = e ? atoi(e) : 0;
   }
+#endif
   p.scale = a.scale;
   p.scale_log2 = a.scale * 1.4426950408889634f;
   const int max_tiles = a.total_q > 0 ? (a.max_seqlen + kBK - 1) / kBK : 0;
@@ -653,9 +660,9 @@ static int launch(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, c
 }
 }  // namespace bwd
 
-int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, cudaStream_t st) {
-  if (!use_v1()) return launch_tc_bwd2(a, self, w, st);
-  return a.head_dim == 64 ? bwd::launch<64>(a, self, w, st) : bwd::launch<128>(a, self, w, st);
+int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, const BwdScratch& w,
+                  cudaStream_t st) {
+  return a.head_dim == 64 ? bwd::launch<64>(a, self, grp, w, st) : bwd::launch<128>(a, self, grp, w, st);
 }
 
 }  // namespace dkv

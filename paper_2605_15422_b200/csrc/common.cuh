@@ -10,6 +10,14 @@
 
 #define DKV_DEVICE __device__ __forceinline__
 
+// Timing-only ablation switches (results are garbage when set): compiled in only for the
+// experiment build (`make trace`, -DDKV_ABLATION); in libdkv.so they are the constant 0.
+#ifdef DKV_ABLATION
+#define DKV_ABL(x) (x)
+#else
+#define DKV_ABL(x) 0
+#endif
+
 namespace dkv {
 
 // ---------------------------------------------------------------- misc

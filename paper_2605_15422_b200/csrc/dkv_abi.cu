@@ -125,6 +125,53 @@ static SimtArgs to_args(const P* p) {
   return a;
 }
 
+// The launch's prompt groups (dkv_group_table, include/dkv.h).  `tc`: the tensor-core kernels
+// serve this shape (multi-group launches need them).  Without `fn` (workspace queries) an
+// invalid table silently degrades to one group -- the launch itself then reports the error.
+template <typename P>
+static int parse_groups(const P* p, bool dualkv, bool tc, GroupTable& g, const char* fn) {
+  const dkv_group_table& t = p->groups;
+  auto bad = [&](const std::string& why) { return fn ? fail(DKV_ERR_INVALID, std::string(fn) + ": " + why) : -1; };
+  g.n = 1;
+  g.seq[0] = 0;
+  g.seq[1] = static_cast<int>(p->num_seqs);
+  g.ctx[0] = 0;
+  g.ctx[1] = static_cast<int>(std::max<int64_t>(0, p->ctx_len));
+  g.max_ctx = g.ctx[1];
+  g.max_seqs = g.seq[1];
+  if (t.num_groups == 0 || t.num_groups == 1) {
+    if (t.num_groups == 1 && t.seq_cu && t.ctx_cu &&
+        (t.seq_cu[0] != 0 || t.seq_cu[1] != p->num_seqs || t.ctx_cu[0] != 0 || t.ctx_cu[1] != p->ctx_len))
+      return bad("group table inconsistent with num_seqs / ctx_len");
+    return DKV_OK;
+  }
+  if (t.num_groups < 0 || t.num_groups > DKV_MAX_GROUPS)
+    return bad("num_groups must be in [0, " + std::to_string(DKV_MAX_GROUPS) + "]");
+  if (!dualkv) return bad("a varlen call takes no group table");
+  if (!t.seq_cu || !t.ctx_cu) return bad("null group table arrays");
+  if (!tc && fn)
+    return fail(DKV_ERR_UNSUPPORTED, std::string(fn) +
+                                         ": multi-group launches run on the tensor-core path only (bf16, "
+                                         "head_dim 64/128)");
+  const int n = static_cast<int>(t.num_groups);
+  if (t.seq_cu[0] != 0 || t.seq_cu[n] != p->num_seqs)
+    return bad("group seq_cu must run from 0 to num_seqs");
+  if (t.ctx_cu[0] != 0 || t.ctx_cu[n] != p->ctx_len) return bad("group ctx_cu must run from 0 to ctx_len");
+  g.n = n;
+  g.max_ctx = 0;
+  g.max_seqs = 0;
+  for (int i = 0; i <= n; ++i) {
+    g.seq[i] = t.seq_cu[i];
+    g.ctx[i] = t.ctx_cu[i];
+    if (i == 0) continue;
+    if (g.seq[i] <= g.seq[i - 1]) return bad("every group needs at least one sequence (seq_cu increasing)");
+    if (g.ctx[i] < g.ctx[i - 1]) return bad("group ctx_cu must be non-decreasing");
+    g.max_ctx = std::max(g.max_ctx, g.ctx[i] - g.ctx[i - 1]);
+    g.max_seqs = std::max(g.max_seqs, g.seq[i] - g.seq[i - 1]);
+  }
+  return DKV_OK;
+}
+
 static int fwd_impl(const dkv_fwd_params* p, bool dualkv, void* stream, const char* fn) {
   int rc = validate_common(p, dualkv, fn);
   if (rc) return rc;
@@ -132,11 +179,15 @@ static int fwd_impl(const dkv_fwd_params* p, bool dualkv, void* stream, const ch
   SimtArgs a = to_args(p);
   a.out = p->out;
   a.lse = p->lse;
+  const bool tc = tc_supported(a.dtype, a.head_dim, a.heads, a.kv_heads);
+  GroupTable grp;
+  rc = parse_groups(p, dualkv, tc, grp, fn);
+  if (rc) return rc;
   auto st = static_cast<cudaStream_t>(stream);
   if (a.total_q == 0) return DKV_OK;
   prof_main_begin(0, st);
-  if (tc_supported(a.dtype, a.head_dim, a.heads, a.kv_heads)) {
-    rc = launch_tc_fwd(a, nullptr, st);
+  if (tc) {
+    rc = launch_tc_fwd(a, nullptr, grp, st);
     if (rc) return rc;
   } else {
     launch_simt_fwd(a, st);
@@ -146,26 +197,44 @@ static int fwd_impl(const dkv_fwd_params* p, bool dualkv, void* stream, const ch
   return check_launch(fn);
 }
 
+// SM count of the current device (queried once per device; B200: 148)
+static int sm_count() {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 148;
+  std::lock_guard<std::mutex> lock(mu);
+  if (static_cast<int>(cache.size()) <= dev) cache.resize(dev + 1, 0);
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
 // context work chunk (sequences per context work unit) for the tensor-core backward
-static int auto_chunk(const dkv_bwd_params* p) {
-  if (p->ctx_chunk > 0) return static_cast<int>(std::min<int64_t>(p->ctx_chunk, p->num_seqs));
+// (chunks never span groups: a chunk is `chunk` consecutive sequences of ONE group)
+static int auto_chunk(const dkv_bwd_params* p, const GroupTable& g) {
+  const int64_t nmax = std::max(1, g.max_seqs);
+  if (p->ctx_chunk > 0) return static_cast<int>(std::min<int64_t>(p->ctx_chunk, nmax));
   {
     static const int env_chunk = [] {  // DKV_CTX_CHUNK: tuning experiments only
       const char* e = getenv("DKV_CTX_CHUNK");
       return e ? atoi(e) : 0;
     }();
-    if (env_chunk > 0) return static_cast<int>(std::min<int64_t>(env_chunk, p->num_seqs));
+    if (env_chunk > 0) return static_cast<int>(std::min<int64_t>(env_chunk, nmax));
   }
-  if (p->ctx_len == 0) return static_cast<int>(p->num_seqs);
+  if (p->ctx_len == 0) return static_cast<int>(nmax);
   const bool tc = tc_bwd_supported(p->dtype, static_cast<int>(p->head_dim), static_cast<int>(p->heads),
                                    static_cast<int>(p->kv_heads));
-  if (!tc) return static_cast<int>(p->num_seqs);  // SIMT: one ordered fold over all sequences
-  // enough context units to fill ~8 waves of 148 SMs, but no more than needed
-  const int64_t n_ctx_tiles = (p->ctx_len + 127) / 128;
-  const int64_t units_per_chunk = n_ctx_tiles * p->kv_heads;
-  int64_t chunks = (148 * 8 + units_per_chunk - 1) / units_per_chunk;
-  chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, p->num_seqs));
-  return static_cast<int>((p->num_seqs + chunks - 1) / chunks);
+  if (!tc) return static_cast<int>(nmax);  // SIMT: one ordered fold over all sequences
+  // enough context units to fill ~8 waves of the SMs, but no more than needed
+  const int64_t n_ctx_tiles = (g.max_ctx + 127) / 128;
+  const int64_t units_per_chunk = std::max<int64_t>(1, n_ctx_tiles * p->kv_heads * g.n);
+  int64_t chunks = (static_cast<int64_t>(sm_count()) * 8 + units_per_chunk - 1) / units_per_chunk;
+  chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, nmax));
+  return static_cast<int>((nmax + chunks - 1) / chunks);
 }
 
 // dpack row padding: per-KV-head row stride a multiple of 4 tokens (16 B TMA stride)
@@ -179,14 +248,14 @@ struct BwdLayout {
 
 // Scratch of one backward launch.  `with_self`: the two-call launch, where Call 1 (the prompt's
 // causal self-attention) runs in the same launch and adds into the same fp32 prompt scratch.
-static BwdLayout bwd_layout(const dkv_bwd_params* p, bool with_self) {
+static BwdLayout bwd_layout(const dkv_bwd_params* p, const GroupTable& g, bool with_self) {
   BwdLayout L{};
   const size_t T = static_cast<size_t>(std::max<int64_t>(0, p->total_q));
   const size_t H = static_cast<size_t>(p->heads), Hk = static_cast<size_t>(std::max<int64_t>(1, p->kv_heads));
   const size_t D = static_cast<size_t>(p->head_dim), P = static_cast<size_t>(std::max<int64_t>(0, p->ctx_len));
   with_self = with_self && P > 0;
-  L.chunk = auto_chunk(p);
-  L.num_chunks = static_cast<int>((p->num_seqs + L.chunk - 1) / L.chunk);
+  L.chunk = auto_chunk(p, g);
+  L.num_chunks = static_cast<int>((std::max(1, g.max_seqs) + L.chunk - 1) / L.chunk);
   L.tc = tc_bwd_supported(p->dtype, static_cast<int>(p->head_dim), static_cast<int>(p->heads),
                           static_cast<int>(p->kv_heads));
   const int writers = L.num_chunks + (with_self ? 1 : 0);  // independent writers of prompt gradients
@@ -223,7 +292,15 @@ static int bwd_impl(const dkv_bwd_params* p, const CtxSelf* self, void* ws, size
   if (self && p->ctx_len > 0 && (!self->q || !self->out || !self->lse || !self->dout || !self->dq))
     return fail(DKV_ERR_INVALID, std::string(fn) + ": null q_ctx/out_ctx/lse_ctx/dout_ctx/dq_ctx");
   const bool with_self = self && p->ctx_len > 0;
-  BwdLayout L = bwd_layout(p, with_self);
+  GroupTable grp;
+  rc = parse_groups(p, dualkv,
+                    tc_bwd_supported(p->dtype, static_cast<int>(p->head_dim), static_cast<int>(p->heads),
+                                     static_cast<int>(p->kv_heads)),
+                    grp, fn);
+  if (rc) return rc;
+  if (grp.n > 1 && p->ctx_partials)
+    return fail(DKV_ERR_INVALID, std::string(fn) + ": ctx_partials is a one-group instrumentation hook");
+  BwdLayout L = bwd_layout(p, grp, with_self);
   if (ws_bytes < L.total || (L.total > 0 && !ws))
     return fail(DKV_ERR_WORKSPACE, std::string(fn) + ": workspace too small (need " + std::to_string(L.total) + ")");
   auto st = static_cast<cudaStream_t>(stream);
@@ -260,6 +337,7 @@ static int bwd_impl(const dkv_bwd_params* p, const CtxSelf* self, void* ws, size
       cudaMemsetAsync(p->dk_ctx, 0, plane * esz, st);
       cudaMemsetAsync(p->dv_ctx, 0, plane * esz, st);
       if (p->ctx_partials) cudaMemsetAsync(p->ctx_partials, 0, L.num_chunks * 2 * plane * 4, st);
+      if (p->ctx_grad_f32) cudaMemsetAsync(p->ctx_grad_f32, 0, 2 * plane * 4, st);
     }
     return check_launch(fn);
   }
@@ -289,7 +367,7 @@ static int bwd_impl(const dkv_bwd_params* p, const CtxSelf* self, void* ws, size
       prof_count(1);
     }
     prof_main_begin(1, st);
-    rc = launch_tc_bwd(a, with_self ? self : nullptr, sc, st);
+    rc = launch_tc_bwd(a, with_self ? self : nullptr, grp, sc, st);
     if (rc) return rc;
     prof_main_end(1, st);
     // the kernel accumulates dQ / softmax_scale (the scale is folded into this single cast)
@@ -320,7 +398,7 @@ static int bwd_impl(const dkv_bwd_params* p, const CtxSelf* self, void* ws, size
     prof_main_end(1, st);
   }
   if (plane > 0) {
-    launch_fold_convert(ctx, L.num_parts, plane, p->dk_ctx, p->dv_ctx, a.dtype, st);
+    launch_fold_convert(ctx, L.num_parts, plane, p->dk_ctx, p->dv_ctx, a.dtype, p->ctx_grad_f32, st);
     prof_count(1);
   }
   return check_launch(fn);
@@ -379,13 +457,19 @@ int32_t dkv_uses_tensor_cores(int32_t dtype, int64_t head_dim, int64_t heads, in
 int32_t dkv_dualkv_fwd(const dkv_fwd_params* p, void* stream) { return fwd_impl(p, true, stream, "dkv_dualkv_fwd"); }
 int32_t dkv_varlen_fwd(const dkv_fwd_params* p, void* stream) { return fwd_impl(p, false, stream, "dkv_varlen_fwd"); }
 
+static GroupTable groups_of(const dkv_bwd_params* p) {
+  GroupTable g;
+  parse_groups(p, true, true, g, nullptr);
+  return g;
+}
+
 size_t dkv_bwd_workspace_size(const dkv_bwd_params* p) {
   if (!p) return 0;
-  return bwd_layout(p, false).total;
+  return bwd_layout(p, groups_of(p), false).total;
 }
 int64_t dkv_bwd_num_ctx_chunks(const dkv_bwd_params* p) {
   if (!p) return 0;
-  return bwd_layout(p, false).num_chunks;
+  return bwd_layout(p, groups_of(p), false).num_chunks;
 }
 int32_t dkv_dualkv_bwd(const dkv_bwd_params* p, void* ws, size_t ws_bytes, void* stream) {
   return bwd_impl(p, nullptr, ws, ws_bytes, true, stream, "dkv_dualkv_bwd");
@@ -405,11 +489,15 @@ int32_t dkv_twocall_fwd(const dkv_twocall_fwd_params* p, void* stream) {
   SimtArgs a = to_args(c);
   a.out = c->out;
   a.lse = c->lse;
+  const bool tc = tc_supported(a.dtype, a.head_dim, a.heads, a.kv_heads);
+  GroupTable grp;
+  rc = parse_groups(c, true, tc, grp, "dkv_twocall_fwd");
+  if (rc) return rc;
   auto st = static_cast<cudaStream_t>(stream);
   CtxSelf self{p->q_ctx, p->out_ctx, p->lse_ctx, nullptr, nullptr};
   prof_main_begin(0, st);
-  if (tc_supported(a.dtype, a.head_dim, a.heads, a.kv_heads)) {
-    rc = launch_tc_fwd(a, c->ctx_len > 0 ? &self : nullptr, st);
+  if (tc) {
+    rc = launch_tc_fwd(a, c->ctx_len > 0 ? &self : nullptr, grp, st);
     if (rc) return rc;
   } else {
     if (a.total_q > 0) launch_simt_fwd(a, st);
@@ -435,7 +523,7 @@ int32_t dkv_twocall_fwd(const dkv_twocall_fwd_params* p, void* stream) {
 
 size_t dkv_twocall_bwd_workspace_size(const dkv_twocall_bwd_params* p) {
   if (!p) return 0;
-  return bwd_layout(&p->call2, true).total;
+  return bwd_layout(&p->call2, groups_of(&p->call2), true).total;
 }
 
 int32_t dkv_twocall_bwd(const dkv_twocall_bwd_params* p, void* ws, size_t ws_bytes, void* stream) {

@@ -49,6 +49,28 @@ struct CtxSelf {
   void* dq;          // backward only
 };
 
+// Prompt groups of one launch (the C ABI's dkv_group_table, validated, with derived maxima).
+// Passed by value inside the kernel parameters (~2 KB); one group = {0, num_seqs} / {0, ctx_len}.
+struct GroupTable {
+  int n;                       // number of groups (>= 1)
+  int max_ctx;                 // max prompt rows of a group
+  int max_seqs;                // max sequences of a group
+  int seq[DKV_MAX_GROUPS + 1]; // sequence ranges
+  int ctx[DKV_MAX_GROUPS + 1]; // prompt row ranges in k_ctx / v_ctx / q_ctx
+  // group of sequence s (binary search; a single group is the common case)
+  __host__ __device__ int group_of(int s) const {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (seq[mid] <= s)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    return lo;
+  }
+};
+
 // profiling hooks (dkv_abi.cu): kind 0 = forward main kernel, 1 = backward main kernel
 void prof_main_begin(int kind, cudaStream_t st);
 void prof_main_end(int kind, cudaStream_t st);
@@ -64,19 +86,20 @@ void launch_simt_bwd(const SimtArgs& a, const float* drow, int chunk, int num_ch
 // D = rowsum(dO*O) into drow [H][T] (SIMT path) and/or the tensor-core path's split-bf16
 // additive-constant rows xsplit [Hk][tpad][G][32] (tpad >= T padding tokens, zero rows)
 void launch_rowsum_do_o(const SimtArgs& a, float* drow, __nv_bfloat16* xsplit, int tpad, cudaStream_t st);
+// f32_out (may be null): also store the folded fp32 sums [2][plane] before the cast
 void launch_fold_convert(const float* partials, int num_parts, int64_t plane, void* dk, void* dv, int dtype,
-                         cudaStream_t st);
+                         float* f32_out, cudaStream_t st);
 void launch_convert(const float* src, void* dst, int dtype, int64_t n, cudaStream_t st, float scale = 1.f);
 
 // sm100 tensor-core paths (fwd_sm100.cu / bwd_sm100.cu)
 bool force_simt();  // DKV_FORCE_SIMT=1: route everything to the SIMT kernels (cross-checks)
 bool tc_supported(int dtype, int head_dim, int heads, int kv_heads);
 bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads);
-int launch_tc_fwd(const SimtArgs& a, const CtxSelf* self, cudaStream_t st);
+int launch_tc_fwd(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, cudaStream_t st);
 // Backward scratch: dq_acc [T,H,D] f32 (pre-zeroed; accumulates dQ / softmax_scale), xsplit from
 // launch_rowsum_do_o; the *_s fields are the fused Call 1's (prompt rows); ctx_acc f32
-// [parts][2][P][Hk][D] pre-zeroed: chunk c writes part c (or every item red.adds part 0 when
-// atomic_ctx), fused Call 1 items write part self_part.
+// [parts][2][P][Hk][D] pre-zeroed: chunk c (of every group) writes part c (or every item red.adds
+// part 0 when atomic_ctx), fused Call 1 items write part self_part.
 struct BwdScratch {
   float* dq_acc;
   const __nv_bfloat16* xsplit;
@@ -88,9 +111,7 @@ struct BwdScratch {
   int chunk, num_chunks, self_part;
   bool atomic_ctx;
 };
-int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, cudaStream_t st);
-// bwd2_sm100.cu: the 128x128-tile backward (experimental, DKV_BWD_V2=1)
-bool tc_bwd2_supported(int head_dim, int heads, int kv_heads);
-int launch_tc_bwd2(const SimtArgs& a, const CtxSelf* self, const BwdScratch& w, cudaStream_t st);
+int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, const BwdScratch& w,
+                  cudaStream_t st);
 
 }  // namespace dkv

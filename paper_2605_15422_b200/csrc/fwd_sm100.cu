@@ -73,6 +73,7 @@ struct Params {
   int n_main_items;       // items >= n_main_items are Call 1 items (causal self-attention over the prompt)
   float scale_log2;       // softmax_scale * log2(e)
   int ablate;             // timing experiments only (DKV_FWD_ABLATE): 1 K/V loads, 2 exponentials
+  GroupTable grp;         // prompt groups of the launch (one group: {0, num_seqs} / {0, ctx_len})
 };
 
 struct Smem {
@@ -108,8 +109,11 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
   // of the two-region problem.  Fused Call 1 items (two-call launch only): the prompt's own
   // queries attend causally to the prompt keys -- one more "sequence" whose own-region K/V are
   // the context tensors and which has no context region.
+  // Multi-group launches: a sequence's context region is its group's prompt rows
+  // [ctx_row0, ctx_row0 + ctx_len) of the concatenated k_ctx / v_ctx; Call 1 items of group g
+  // run the prompt rows of that group.
   const bool self_item = item >= p.n_main_items;
-  int hk, jb, seq0, rlen, n_ctx, lse_stride;
+  int hk, jb, seq0, rlen, n_ctx, lse_stride, ctx_row0 = 0, ctx_len = 0;
   const CUtensorMap *mq, *mk_own, *mv_own;
   __nv_bfloat16* out;
   float* lse_out;
@@ -120,7 +124,10 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     jb = rest / p.num_seqs;
     seq0 = p.cu[seq];
     rlen = p.cu[seq + 1] - seq0;
-    n_ctx = (p.ctx_len + kBN - 1) / kBN;
+    const int g = p.grp.group_of(seq);
+    ctx_row0 = p.grp.ctx[g];
+    ctx_len = p.grp.ctx[g + 1] - ctx_row0;
+    n_ctx = (ctx_len + kBN - 1) / kBN;
     mq = &p.tm_q;
     mk_own = &p.tm_k;
     mv_own = &p.tm_v;
@@ -130,9 +137,11 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
   } else {
     const int b = item - p.n_main_items;
     hk = b % p.kv_heads;
-    jb = b / p.kv_heads;
-    seq0 = 0;
-    rlen = p.ctx_len;
+    const int rest = b / p.kv_heads;
+    const int g = rest % p.grp.n;
+    jb = rest / p.grp.n;
+    seq0 = p.grp.ctx[g];
+    rlen = p.grp.ctx[g + 1] - seq0;
     n_ctx = 0;
     mq = &p.tm_qs;
     mk_own = &p.tm_kc;
@@ -236,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         const uint32_t ph = (it / kSt) & 1;
         const CUtensorMap* mk = is_ctx ? &p.tm_kc : mk_own;
         const CUtensorMap* mv = is_ctx ? &p.tm_vc : mv_own;
-        const int row = is_ctx ? j * kBN : seq0 + j * kBN;
+        const int row = is_ctx ? ctx_row0 + j * kBN : seq0 + j * kBN;
         mbar_wait(&sm.k_empty[slot], ph ^ 1);
         TRACE(T_Q_LOAD, it);
         if constexpr (kPair) {
@@ -254,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
                           hk, row);
           continue;
         }
-        const bool skip_kv = (p.ablate & 1) || ((p.ablate & 4) && it >= C::kStages);  // 4: reuse the first tiles
+        const bool skip_kv = (DKV_ABL(p.ablate) & 1) || ((DKV_ABL(p.ablate) & 4) && it >= C::kStages);  // 4: reuse the first tiles
         mbar_arrive_expect_tx(&sm.k_full[slot], skip_kv ? 0 : C::kTileBytes);
         for (int pn = 0; pn < C::kPanels && !skip_kv; ++pn)
           tma_load_3d_hint(sK + slot * C::kTileBytes + pn * C::kPanelBytes, mk, &sm.k_full[slot], pn * 64, hk,
@@ -403,9 +412,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         // masks: own tiles on/after the tile's first token are causal; the last
         // context tile may be partial (keys >= P are out of bounds)
         const int kbase = j * kBN + cb;
-        const bool need_mask = is_ctx ? (kbase + 64 > p.ctx_len) : (kbase + 63 > qmin);
+        const bool need_mask = is_ctx ? (kbase + 64 > ctx_len) : (kbase + 63 > qmin);
         if (need_mask) {
-          const int lim = is_ctx ? p.ctx_len - 1 - kbase : qtok - kbase;  // last visible column
+          const int lim = is_ctx ? ctx_len - 1 - kbase : qtok - kbase;  // last visible column
 #pragma unroll
           for (int c = 0; c < 64; ++c)
             if (c > lim) s[c] = -INFINITY;
@@ -445,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
           for (int i = 0; i < 16; ++i) {
             const float2 x = __ffma2_rn(make_float2(s[c0 + 2 * i], s[c0 + 2 * i + 1]), sc2, nm2);
             float2 e;
-            if (p.ablate & 2) {
+            if (DKV_ABL(p.ablate) & 2) {
               e = x;
             } else if (i >= 16 - kPolyPairs) {
               e = ex2_poly2(x);
@@ -537,9 +546,10 @@ static bool fwd_pairs() {
 }
 
 template <int D>
-int launch(const SimtArgs& a, const CtxSelf* self, cudaStream_t st) {
+int launch(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, cudaStream_t st) {
   using C = Cfg<D>;
   Params p{};
+  p.grp = grp;
   const int G = a.heads / a.kv_heads;
   const int tq = kBM / G;
   if (a.total_q > 0 &&
@@ -580,14 +590,17 @@ int launch(const SimtArgs& a, const CtxSelf* self, cudaStream_t st) {
   p.group = G;
   p.tq = tq;
   p.scale_log2 = a.scale * 1.4426950408889634f;
+#ifdef DKV_ABLATION  // timing-experiment builds only (libdkv_trace.so); never read by libdkv.so
   {
     const char* e = getenv("DKV_FWD_ABLATE");
     p.ablate = e ? atoi(e) : 0;
   }
+#endif
   const int span = (pair ? 4 : 2) * tq;  // tokens per work item (a CTA, or a CTA pair)
   const int blocks_per_seq = a.total_q > 0 ? (a.max_seqlen + span - 1) / span : 0;
   const int64_t main_items = static_cast<int64_t>(blocks_per_seq) * a.num_seqs * a.kv_heads;
-  const int64_t self_items = with_self ? static_cast<int64_t>((a.ctx_len + span - 1) / span) * a.kv_heads : 0;
+  const int64_t self_items =
+      with_self ? static_cast<int64_t>((grp.max_ctx + span - 1) / span) * grp.n * a.kv_heads : 0;
   const int64_t items = main_items + self_items;  // Call 1 items run in the tail of Call 2's
   if (items == 0) return DKV_OK;
   if (items * (pair ? 2 : 1) > 0x7fffffff) {
@@ -644,9 +657,9 @@ bool tc_supported(int dtype, int head_dim, int heads, int kv_heads) {
   return G <= 128 && (128 % G) == 0;
 }
 
-int launch_tc_fwd(const SimtArgs& a, const CtxSelf* self, cudaStream_t st) {
-  if (a.head_dim == 128) return fwd::launch<128>(a, self, st);
-  return fwd::launch<64>(a, self, st);
+int launch_tc_fwd(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, cudaStream_t st) {
+  if (a.head_dim == 128) return fwd::launch<128>(a, self, grp, st);
+  return fwd::launch<64>(a, self, grp, st);
 }
 
 }  // namespace dkv

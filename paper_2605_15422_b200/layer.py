@@ -3,56 +3,119 @@
 
 `DualKVSelfAttention` is what a trainer swaps in (the paper's veRL monkey-patch installs the same
 call on supported model classes): QKV projections run once per prompt token (plain
-library GEMMs on the P+NR rows -- the rho saving), RoPE rotates rows at their LOGICAL positions
-(prompt j -> j, response r -> P + r), and each prompt group runs the fused two-call op (Call 1
-over the prompt, Call 2 over the responses, one fp32 prompt-KV gradient cast once).  Autograd
-covers the whole block; parameter gradients are what `dp.GradSync` all-reduces.
+library GEMMs on the P+NR rows -- the rho saving), Qwen3's per-head RMSNorm of q and k (optional,
+`qk_norm=True`; the reference toy model has none), RoPE rotates rows at their LOGICAL
+positions (prompt j -> j, response r -> P + r), and ALL prompt groups of the micro-batch run in ONE
+fused two-call launch (Call 1 over every prompt, Call 2 over every response, each group's prompt
+K/V gradient accumulated in fp32 and cast once) -- the reference loops over groups
+(layer.py:239).  Every device op is a registered torch.library op, so the block compiles with
+`torch.compile(fullgraph=True)`; parameter gradients are what `dp.GradSync` all-reduces.
 """
 
 from __future__ import annotations
 
 import math
+from dataclasses import dataclass
+from typing import List, Union
 
+import numpy as np
 import torch
 
-from .api import dualkv_two_call_attention
-from .packing import PackPlan
-from .rope import RoPE, dualkv_positions
+from . import library  # noqa: F401  (registers the dualkv:: ops)
+from ._lib import DKV_MAX_GROUPS
+from .packing import PackPlan, position_ids
 
-__all__ = ["DualKVSelfAttention"]
+__all__ = ["DualKVSelfAttention", "DualKVBatch"]
+
+
+@dataclass
+class DualKVBatch:
+    """Device metadata of one P+NR micro-batch, built once per layout (outside any compiled region).
+
+    The packed rows keep the reference layout (per group [prompt; responses], packing.py:182-220);
+    the single launch takes every prompt and every response as two contiguous row sets, picked
+    with `ctx_rows` / `resp_rows` and put back with `inv_perm`."""
+
+    total: int
+    positions: torch.Tensor   # [T_dk] int64 logical positions (packing.py:105-120)
+    ctx_rows: torch.Tensor    # [sum P_g] int64 packed rows of the prompts, group order
+    resp_rows: torch.Tensor   # [sum R] int64 packed rows of the responses
+    inv_perm: torch.Tensor    # [T_dk] int64: row of cat(prompts, responses) holding packed row i
+    cu_seqlens: torch.Tensor  # [N+1] int32 response offsets over all groups
+    max_seqlen: int
+    group_seq_cu: List[int]
+    group_ctx_cu: List[int]
+
+    @staticmethod
+    def from_plan(plan: PackPlan, device) -> "DualKVBatch":
+        key = ("dualkv_batch", str(device))
+        if key in plan._dev:
+            return plan._dev[key]
+        if len(plan.groups) > DKV_MAX_GROUPS:
+            raise ValueError(f"at most {DKV_MAX_GROUPS} prompt groups per launch")
+        ctx_rows, resp_rows, lens, gs, gc = [], [], [], [0], [0]
+        for g in plan.groups:
+            ctx_rows.append(g.context_start + np.arange(g.prompt_len))
+            resp_rows.append(g.resp_start + np.arange(int(g.resp_cu[-1])))
+            lens.extend(int(r) for r in g.resp_lens)
+            gs.append(gs[-1] + len(g.resp_lens))
+            gc.append(gc[-1] + g.prompt_len)
+        ctx_rows = np.concatenate(ctx_rows).astype(np.int64)
+        resp_rows = np.concatenate(resp_rows).astype(np.int64)
+        order = np.concatenate([ctx_rows, resp_rows])
+        inv = np.empty_like(order)
+        inv[order] = np.arange(order.size)
+        cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        t = lambda a, dt=torch.int64: torch.as_tensor(a, dtype=dt, device=device)
+        b = DualKVBatch(plan.total_dualkv, t(position_ids(plan, "dualkv")), t(ctx_rows), t(resp_rows), t(inv),
+                        t(cu, torch.int32), int(max(lens)) if lens else 0, gs, gc)
+        plan._dev[key] = b
+        return b
+
+
+def _rms_norm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
+    """Per-head RMSNorm over head_dim (Qwen3 q_norm / k_norm), fp32 statistics."""
+    xf = x.float()
+    return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps) * w.float()).to(x.dtype)
 
 
 class DualKVSelfAttention(torch.nn.Module):
     def __init__(self, d_model: int, heads: int, kv_heads: int, head_dim: int, rope_base: float = 10000.0,
-                 dtype=torch.bfloat16, device="cuda"):
+                 dtype=torch.bfloat16, device="cuda", qk_norm: bool = False, eps: float = 1e-6):
         super().__init__()
         if heads % kv_heads:
             raise ValueError("heads must be a multiple of kv_heads")
-        self.h, self.hk, self.d, self.base = heads, kv_heads, head_dim, rope_base
+        self.h, self.hk, self.d, self.base, self.eps = heads, kv_heads, head_dim, float(rope_base), eps
+        self.scale = 1.0 / math.sqrt(head_dim)
         mk = lambda i, o: torch.nn.Parameter(
             (torch.randn(i, o, device=device) / math.sqrt(i)).to(dtype))
         self.w_q, self.w_k, self.w_v = mk(d_model, heads * head_dim), mk(d_model, kv_heads * head_dim), \
             mk(d_model, kv_heads * head_dim)
         self.w_o = mk(heads * head_dim, d_model)
+        self.qk_norm = qk_norm
+        if qk_norm:
+            self.q_norm = torch.nn.Parameter(torch.ones(head_dim, device=device, dtype=dtype))
+            self.k_norm = torch.nn.Parameter(torch.ones(head_dim, device=device, dtype=dtype))
 
-    def forward(self, x: torch.Tensor, plan: PackPlan) -> torch.Tensor:
-        """x: [T_dk, d_model] hidden states of the P+NR rows of `plan`; returns the block's output
-        projection [T_dk, d_model] (no residual)."""
-        if x.shape[0] != plan.total_dualkv:
-            raise ValueError(f"expected {plan.total_dualkv} rows, got {x.shape[0]}")
+    def forward(self, x: torch.Tensor, batch: Union[DualKVBatch, PackPlan]) -> torch.Tensor:
+        """x: [T_dk, d_model] hidden states of the P+NR rows; returns the block's output projection
+        [T_dk, d_model] (no residual)."""
+        if isinstance(batch, PackPlan):
+            batch = DualKVBatch.from_plan(batch, x.device)
+        if x.shape[0] != batch.total:
+            raise ValueError(f"expected {batch.total} rows, got {x.shape[0]}")
         t = x.shape[0]
-        pos = dualkv_positions(plan, x.device)
-        q = RoPE.apply((x @ self.w_q).view(t, self.h, self.d), pos, self.base)
-        k = RoPE.apply((x @ self.w_k).view(t, self.hk, self.d), pos, self.base)
+        q = (x @ self.w_q).view(t, self.h, self.d)
+        k = (x @ self.w_k).view(t, self.hk, self.d)
         v = (x @ self.w_v).view(t, self.hk, self.d)
-        outs = []
-        for g in plan.groups:
-            c0, c1 = g.context_start, g.context_start + g.prompt_len
-            r0, r1 = g.resp_start, g.resp_start + int(g.resp_cu[-1])
-            if g.prompt_len == 0 or r1 == r0:
-                raise ValueError("DualKVSelfAttention needs P > 0 and at least one response token per group")
-            oc, od = dualkv_two_call_attention(q[c0:c1], k[c0:c1], v[c0:c1], q[r0:r1], k[r0:r1], v[r0:r1],
-                                               g.resp_cu)
-            outs += [oc, od]
-        o = torch.cat(outs, dim=0).reshape(t, self.h * self.d)
+        if self.qk_norm:
+            q, k = _rms_norm(q, self.q_norm, self.eps), _rms_norm(k, self.k_norm, self.eps)
+        q = torch.ops.dualkv.rope(q.contiguous(), batch.positions, self.base, False)
+        k = torch.ops.dualkv.rope(k.contiguous(), batch.positions, self.base, False)
+        pick = lambda a, rows: a.index_select(0, rows)
+        o_c, _, o_d, _ = torch.ops.dualkv.two_call_fwd(
+            pick(q, batch.ctx_rows), pick(k, batch.ctx_rows), pick(v, batch.ctx_rows),
+            pick(q, batch.resp_rows), pick(k, batch.resp_rows), pick(v, batch.resp_rows),
+            batch.cu_seqlens, batch.max_seqlen, self.scale, batch.group_seq_cu, batch.group_ctx_cu)
+        o = torch.cat([o_c, o_d], dim=0).index_select(0, batch.inv_perm).reshape(t, self.h * self.d)
         return o @ self.w_o

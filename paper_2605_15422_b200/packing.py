@@ -76,6 +76,10 @@ def make_plan(groups: Sequence[Tuple[int, Sequence[int]]]) -> PackPlan:
         rs = [int(r) for r in rs]
         if p_len < 0 or any(r < 0 for r in rs):
             raise ValueError("negative length")
+        if not rs:
+            # the reference rejects a rollout group with no responses (RolloutGroup.__post_init__);
+            # its prompt rows would otherwise have no copy to come from
+            raise ValueError("a prompt group needs at least one response")
         seq_cu = np.concatenate([[0], np.cumsum([p_len + r for r in rs])]).astype(np.int64) + std_cur
         resp_cu = np.concatenate([[0], np.cumsum(rs)]).astype(np.int64)
         ctx0, rs0 = dk_cur, dk_cur + p_len
@@ -104,8 +108,8 @@ def make_plan(groups: Sequence[Tuple[int, Sequence[int]]]) -> PackPlan:
                     np.concatenate([[0], np.cumsum(seg_lens)]).astype(np.int64), cat(seg_src))
 
 
-def _stream():
-    return torch.cuda.current_stream().cuda_stream
+def _stream(device):
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 def _gather(x: torch.Tensor, idx: torch.Tensor, n_out: int) -> torch.Tensor:
@@ -113,8 +117,9 @@ def _gather(x: torch.Tensor, idx: torch.Tensor, n_out: int) -> torch.Tensor:
     out = torch.empty((n_out,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
     row_bytes = x[0].numel() * x.element_size() if x.shape[0] else 0
     if n_out and row_bytes:
-        check(lib.dkv_gather_rows(x.data_ptr(), out.data_ptr(), row_bytes, idx.data_ptr(), n_out, _stream()),
-              "gather_rows")
+        with torch.cuda.device(x.device):
+            check(lib.dkv_gather_rows(x.data_ptr(), out.data_ptr(), row_bytes, idx.data_ptr(), n_out,
+                                      _stream(x.device)), "gather_rows")
     return out
 
 
@@ -142,10 +147,11 @@ def reduce_to_dualkv(g_std: torch.Tensor, plan: PackPlan) -> torch.Tensor:
     out = torch.empty((plan.total_dualkv,) + tuple(g_std.shape[1:]), dtype=g_std.dtype, device=g_std.device)
     row = g_std[0].numel() if g_std.shape[0] else 0
     if plan.total_dualkv and row:
-        check(lib.dkv_segment_sum_rows(
-            g_std.data_ptr(), out.data_ptr(), DKV_F32 if g_std.dtype == torch.float32 else DKV_BF16, row,
-            plan.device("seg", g_std.device).data_ptr(), plan.device("seg_src", g_std.device).data_ptr(),
-            plan.total_dualkv, _stream()), "segment_sum_rows")
+        with torch.cuda.device(g_std.device):
+            check(lib.dkv_segment_sum_rows(
+                g_std.data_ptr(), out.data_ptr(), DKV_F32 if g_std.dtype == torch.float32 else DKV_BF16, row,
+                plan.device("seg", g_std.device).data_ptr(), plan.device("seg_src", g_std.device).data_ptr(),
+                plan.total_dualkv, _stream(g_std.device)), "segment_sum_rows")
     return out
 
 

@@ -25,8 +25,8 @@ __all__ = ["rope_logical", "RoPE", "repack_rope_to_dualkv", "dualkv_positions"]
 _DT = {torch.bfloat16: DKV_BF16, torch.float32: DKV_F32}
 
 
-def _stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 def dualkv_positions(plan: PackPlan, device) -> torch.Tensor:
@@ -57,10 +57,13 @@ def _rope_rows(x: torch.Tensor, pos: torch.Tensor, base: float, inverse: bool,
         raise ValueError(f"rope: expected [T, heads, even head_dim], got {tuple(x.shape)}")
     x = x.contiguous()
     n = x.shape[0] if n_out is None else n_out
-    out = torch.empty((n,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
-    check(lib.dkv_rope_rows(x.data_ptr(), out.data_ptr(), _DT[x.dtype], n, x.shape[1], x.shape[2],
-                            pos.data_ptr() if n else None, None if idx is None else idx.data_ptr(),
-                            float(base), int(inverse), _stream()), "rope_rows")
+    if pos.device != x.device or pos.dtype != torch.int64 or pos.dim() != 1 or pos.shape[0] != n:
+        raise ValueError(f"rope: positions must be int64 [{n}] on {x.device}")
+    with torch.cuda.device(x.device):
+        out = torch.empty((n,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        check(lib.dkv_rope_rows(x.data_ptr(), out.data_ptr(), _DT[x.dtype], n, x.shape[1], x.shape[2],
+                                pos.data_ptr() if n else None, None if idx is None else idx.data_ptr(),
+                                float(base), int(inverse), _stream(x.device)), "rope_rows")
     return out
 
 
@@ -70,20 +73,14 @@ def rope_logical(x: torch.Tensor, positions, base: float = 10000.0, inverse: boo
     return _rope_rows(x, _as_positions(positions, x.shape[0], x.device), base, inverse)
 
 
-class RoPE(torch.autograd.Function):
-    """y = rope(x, positions); dx = rope_bwd(dy, positions) (an orthogonal rotation)."""
+class RoPE:
+    """y = rope(x, positions); dx = rope_bwd(dy, positions) (an orthogonal rotation) -- the
+    registered op `dualkv::rope` (library.py), autograd-enabled and torch.compile-traceable."""
 
     @staticmethod
-    def forward(ctx, x, positions, base=10000.0):
-        pos = _as_positions(positions, x.shape[0], x.device)
-        ctx.save_for_backward(pos)
-        ctx.base = base
-        return _rope_rows(x, pos, base, False)
-
-    @staticmethod
-    def backward(ctx, dy):
-        (pos,) = ctx.saved_tensors
-        return _rope_rows(dy, pos, ctx.base, True), None, None
+    def apply(x, positions, base=10000.0):
+        from .library import rope
+        return rope(x, _as_positions(positions, x.shape[0], x.device), base)
 
 
 def repack_rope_to_dualkv(q_std: torch.Tensor, k_std: torch.Tensor, v_std: torch.Tensor, plan: PackPlan,
@@ -95,7 +92,8 @@ def repack_rope_to_dualkv(q_std: torch.Tensor, k_std: torch.Tensor, v_std: torch
         if x.shape[0] != plan.total_standard:
             raise ValueError(f"{name}: expected {plan.total_standard} rows, got {x.shape[0]}")
     for x in (q_std, k_std, v_std):
-        if not x.is_cuda or x.dtype not in _DT or x.dim() != 3 or x.dtype != q_std.dtype:
+        if not x.is_cuda or x.dtype not in _DT or x.dim() != 3 or x.dtype != q_std.dtype \
+                or x.device != q_std.device:
             raise ValueError("repack_rope_to_dualkv: CUDA [T, heads, d] bf16/fp32 tensors of one dtype")
     if k_std.shape != v_std.shape or k_std.shape[2] != q_std.shape[2]:
         raise ValueError("repack_rope_to_dualkv: k / v shapes inconsistent with q")
@@ -103,12 +101,16 @@ def repack_rope_to_dualkv(q_std: torch.Tensor, k_std: torch.Tensor, v_std: torch
     idx = plan.device("dk_from_std", q_std.device)
     pos = dualkv_positions(plan, q_std.device)
     n = plan.total_dualkv
+    if pos.shape[0] != n or idx.shape[0] != n:
+        raise ValueError(f"repack plan inconsistent: {pos.shape[0]} positions / {idx.shape[0]} rows for "
+                         f"{n} packed rows")
     q = torch.empty((n,) + tuple(q_std.shape[1:]), dtype=q_std.dtype, device=q_std.device)
     k = torch.empty((n,) + tuple(k_std.shape[1:]), dtype=k_std.dtype, device=k_std.device)
     v = torch.empty_like(k)
     if n:
-        check(lib.dkv_rope_qkv_rows(q_std.data_ptr(), k_std.data_ptr(), v_std.data_ptr(), q.data_ptr(),
-                                    k.data_ptr(), v.data_ptr(), _DT[q_std.dtype], n, q_std.shape[1],
-                                    k_std.shape[1], q_std.shape[2], pos.data_ptr(), idx.data_ptr(), float(base),
-                                    0, _stream()), "rope_qkv_rows")
+        with torch.cuda.device(q_std.device):
+            check(lib.dkv_rope_qkv_rows(q_std.data_ptr(), k_std.data_ptr(), v_std.data_ptr(), q.data_ptr(),
+                                        k.data_ptr(), v.data_ptr(), _DT[q_std.dtype], n, q_std.shape[1],
+                                        k_std.shape[1], q_std.shape[2], pos.data_ptr(), idx.data_ptr(),
+                                        float(base), 0, _stream(q_std.device)), "rope_qkv_rows")
     return q, k, v

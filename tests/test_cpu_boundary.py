@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), f"libdkv.so does not export {name}"
     assert set(declared) == set(_lib.SIGNATURES), "ctypes signatures out of sync with include/dkv.h"
-    assert _lib.lib.dkv_abi_version() == 1
+    assert _lib.lib.dkv_abi_version() == _lib.DKV_ABI_VERSION == 2
 
 
 def test_validation_errors_without_gpu():

@@ -83,3 +83,45 @@ def test_gradient_allreduce_world2_matches_single_process():
     assert owned == list(range(len(GROUPS)))
     for r in range(world):
         np.testing.assert_allclose(out[r][1], total, rtol=1e-12, atol=1e-12)
+
+
+def _worker_overlap(rank, world, port, out):
+    """bf16 parameters, hooks launching the all-reduce from inside backward (overlap=True):
+    the synced gradient is the fp32 sum of the ranks' gradients cast to bf16 ONCE."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_15422_b200.dp import GradSync
+    torch.manual_seed(0)
+    w1 = torch.nn.Parameter(torch.randn(16, 8).to(torch.bfloat16))
+    w2 = torch.nn.Parameter(torch.randn(8, 4).to(torch.bfloat16))
+    sync = GradSync([w1, w2], bucket_bytes=16 * 8 * 4, overlap=True)  # two buckets
+    g = torch.Generator().manual_seed(10 + rank)
+    x = torch.randn(32, 16, generator=g).to(torch.bfloat16)
+    with sync.no_sync():  # an earlier micro-batch: accumulate locally, no collective
+        ((x @ w1) @ w2).float().pow(2).sum().backward()
+    assert not sync._pending
+    local = [w1.grad.float().clone(), w2.grad.float().clone()]
+    w1.grad = None
+    w2.grad = None
+    ((x @ w1) @ w2).float().pow(2).sum().backward()   # hooks launch both buckets here
+    launched = sorted(sync._pending)
+    local2 = [w1.grad.float().clone(), w2.grad.float().clone()]
+    sync.sync()
+    out[rank] = (launched, [l.numpy() for l in local2], [w1.grad.float().numpy(), w2.grad.float().numpy()],
+                 [w1.grad.dtype, w2.grad.dtype])
+    dist.destroy_process_group()
+
+
+def test_overlapped_bf16_gradient_sync_world2():
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_overlap, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        launched, _, synced, dts = out[r]
+        assert launched == [0, 1], "both buckets launched from the backward hooks"
+        assert dts == [torch.bfloat16, torch.bfloat16]
+        for i in range(2):
+            exact = out[0][1][i].astype(np.float64) + out[1][1][i].astype(np.float64)
+            want = torch.from_numpy(exact.astype(np.float32)).to(torch.bfloat16).float().numpy()
+            np.testing.assert_array_equal(synced[i], want)  # fp32 sum, one cast

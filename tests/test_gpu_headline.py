@@ -1,0 +1,122 @@
+"""Parity at the BASELINE headline configs, through EXACTLY the call bench.py times.
+
+bench.py's step is `dualkv_two_call_fwd` + `dualkv_two_call_bwd(..., deterministic=False)` (the
+atomic prompt-gradient merge).  Here the same call at full C3 (N=32, P=8K, R=2K, H=32/8, d=128)
+and C5 (N=32, P=16K, R=2K, H=32/4) is checked against an INDEPENDENT dense float64 reference
+(torch on the GPU, `gpu_helpers.ref_attention_slice_f64`; SURVEY §8c oracle 1 on a slice):
+
+* the first and the last sequence x the first and the last KV-head group: O, lse, dQ, dK_d, dV_d;
+* the TOTAL prompt gradient dK_c / dV_c of those KV heads: the f64 sum over all N sequences of
+  their prompt-key gradients plus Call 1's (the prompt's causal self-attention);
+* SURVEY §8c bounds: bf16 |gpu-ref| <= 1e-2 + 1e-2|ref| elementwise and max-relative <= 1e-2,
+  lse <= 1e-3 absolute.
+
+And the atomic merge against the ordered fold (verify.py:325-355, test_dualkv.py:183): the fp32
+prompt gradient (before its cast) of `deterministic=False` vs `deterministic=True` differs by at
+most 4 fp32 ulp at accumulation scale (the sum of the per-sequence contribution magnitudes).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from gpu_helpers import LSE_ATOL, assert_bf16_vs_f64, ref_attention_slice_f64
+
+pytestmark = pytest.mark.gpu
+
+CFGS = {"C3": (32, 8192, 2048, 32, 8), "C5": (32, 16384, 2048, 32, 4)}
+
+
+def _rand(g, *shape):
+    return torch.randn(*shape, device="cuda", generator=g).to(torch.bfloat16)
+
+
+def _inputs(cfg, seed):
+    n, p, r, h, hk = cfg
+    d = 128
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    t = n * r
+    qc, kc, vc, doc = _rand(g, p, h, d), _rand(g, p, hk, d), _rand(g, p, hk, d), _rand(g, p, h, d)
+    q, kd, vd, dod = _rand(g, t, h, d), _rand(g, t, hk, d), _rand(g, t, hk, d), _rand(g, t, h, d)
+    cu = np.arange(0, t + 1, r, dtype=np.int64)
+    return qc, kc, vc, doc, q, kd, vd, dod, cu
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_bench_call_vs_f64_slices(name, cuda_device):
+    import paper_2605_15422_b200 as dkv
+    torch.backends.cuda.matmul.allow_tf32 = False
+    n, p, r, h, hk = CFGS[name]
+    d, G = 128, h // hk
+    scale = 1.0 / np.sqrt(d)
+    qc, kc, vc, doc, q, kd, vd, dod, cu = _inputs(CFGS[name], 21)
+    inp = dkv.DualKVInput(q, kc, vc, kd, vd, cu)
+    # --- exactly bench.py's step
+    oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc, inp)
+    dq_c, dkc, dvc, dq, dkd, dvd = dkv.dualkv_two_call_bwd(qc, inp, oc, lc, doc, od, ld, dod, deterministic=False)
+    torch.cuda.synchronize()
+    worst = {}
+    for kh in (0, hk - 1):
+        heads = slice(kh * G, (kh + 1) * G)
+        dk_tot = torch.zeros(p, d, dtype=torch.float64, device="cuda")
+        dv_tot = torch.zeros_like(dk_tot)
+        for s in range(n):
+            a, b = int(cu[s]), int(cu[s + 1])
+            keys = torch.cat([kc[:, kh], kd[a:b, kh]])
+            vals = torch.cat([vc[:, kh], vd[a:b, kh]])
+            o_r, lse_r, dq_r, dk_r, dv_r = ref_attention_slice_f64(q[a:b, heads], keys, vals, dod[a:b, heads], p,
+                                                                   scale)
+            dk_tot += dk_r[:p]
+            dv_tot += dv_r[:p]
+            if s in (0, n - 1):
+                tag = f"{name} seq {s} kv head {kh}"
+                worst[f"O {tag}"] = assert_bf16_vs_f64(od[a:b, heads], o_r, f"O {tag}")
+                lse_err = (ld[heads, a:b].double() - lse_r).abs().max().item()
+                assert lse_err <= LSE_ATOL, f"lse {tag}: {lse_err:.3e}"
+                worst[f"dQ {tag}"] = assert_bf16_vs_f64(dq[a:b, heads], dq_r, f"dQ {tag}")
+                worst[f"dK_d {tag}"] = assert_bf16_vs_f64(dkd[a:b, kh], dk_r[p:], f"dK_d {tag}")
+                worst[f"dV_d {tag}"] = assert_bf16_vs_f64(dvd[a:b, kh], dv_r[p:], f"dV_d {tag}")
+            del o_r, lse_r, dq_r, dk_r, dv_r
+        # Call 1: the prompt's own causal self-attention over the single prompt copy
+        o1, lse1, dq1, dk1, dv1 = ref_attention_slice_f64(qc[:, heads], kc[:, kh], vc[:, kh], doc[:, heads], 0,
+                                                          scale)
+        worst[f"O_ctx kv head {kh}"] = assert_bf16_vs_f64(oc[:, heads], o1, f"{name} O_ctx kv head {kh}")
+        assert (lc[heads].double() - lse1).abs().max().item() <= LSE_ATOL
+        worst[f"dQ_ctx kv head {kh}"] = assert_bf16_vs_f64(dq_c[:, heads], dq1, f"{name} dQ_ctx kv head {kh}")
+        worst[f"dK_c kv head {kh}"] = assert_bf16_vs_f64(dkc[:, kh], dk_tot + dk1, f"{name} dK_c total kv head {kh}")
+        worst[f"dV_c kv head {kh}"] = assert_bf16_vs_f64(dvc[:, kh], dv_tot + dv1, f"{name} dV_c total kv head {kh}")
+        del o1, lse1, dq1, dk1, dv1
+    print(f"{name} max-relative errors vs f64:", {k: round(v, 5) for k, v in worst.items()})
+    del qc, kc, vc, doc, q, kd, vd, dod, oc, lc, od, ld, dq_c, dkc, dvc, dq, dkd, dvd
+    torch.cuda.empty_cache()
+
+
+def test_atomic_merge_within_4_ulp_of_ordered_fold_c3(cuda_device):
+    """The bench's atomic prompt-gradient merge vs the reference's ordered fold at full C3."""
+    import paper_2605_15422_b200 as dkv
+    _, kc, vc, _, q, kd, vd, dod, cu = _inputs(CFGS["C3"], 22)
+    inp = dkv.DualKVInput(q, kc, vc, kd, vd, cu)
+    o, lse = dkv.dualkv_fwd(inp)
+    det = dkv.dualkv_bwd(inp, o, lse, dod, deterministic=True, return_context_f32=True)
+    ato = [dkv.dualkv_bwd(inp, o, lse, dod, deterministic=False, return_context_f32=True) for _ in range(2)]
+    contribs = dkv.context_grad_contributions(inp, o, lse, dod)
+    torch.cuda.synchronize()
+    assert len(contribs) == 32
+    scale_k = sum(c[0].abs() for c in contribs)
+    scale_v = sum(c[1].abs() for c in contribs)
+    worst = 0.0
+    for run in ato:
+        for which, acc_scale in ((0, scale_k), (1, scale_v)):
+            ulp = torch.nextafter(acc_scale, torch.full_like(acc_scale, float("inf"))) - acc_scale
+            diff = (run[5][which].double() - det[5][which].double()).abs()
+            worst = max(worst, (diff / ulp.double()).max().item())
+        # the cast happens once, after the merge: the bf16 outputs are the fp32 totals rounded once
+        assert torch.equal(run[1], run[5][0].to(torch.bfloat16)) and torch.equal(run[2], run[5][1].to(torch.bfloat16))
+    assert worst <= 4.0, f"atomic vs ordered fold: {worst:.2f} fp32 ulp at accumulation scale"
+    # the decoded-region outputs never merge across items: identical in both modes
+    assert torch.equal(ato[0][3], det[3]) and torch.equal(ato[0][4], det[4])
+    # and the per-sequence contributions add up to the ordered total: the two differ only by fp32
+    # reassociation inside the tensor-core accumulators (a few hundred adds per element)
+    total_k = sum(c[0].double() for c in contribs)
+    rel = ((total_k - det[5][0].double()).abs() / scale_k.double().clamp_min(1e-30)).max().item()
+    assert rel <= 256 * 2 ** -23, f"contributions vs ordered total: {rel:.3e} of the accumulation scale"
