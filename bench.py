@@ -7,10 +7,20 @@ tokens each, H=32 query / H_k=8 KV heads, d=128, bf16.  One step = Call 1
 two-region DualKV) forward AND backward -- the reference's `run_bench` "dk"
 unit (src/bench.py:146-152).  value = algorithmic TFLOP/s
 (14 * visible_pairs * H * d per step), whole job over all ranks.
+All of a rank's prompt groups run in ONE forward and ONE backward launch
+(the group table, include/dkv.h).
+
+Other BASELINE configs (`--config`): C1 (fp32, latency-bound: reports us),
+C2, C5 (8 groups per GPU, one launch) and C4 -- 64 DAPO groups with ragged
+responses, LPT over the ranks, whose step is a whole attention LAYER in the
+P+NR layout: device repack of the micro-batch's input rows, QKV projection,
+Qwen3 q/k RMSNorm, RoPE at logical positions, the multi-group two-call op,
+output projection, backward, and the overlapped fp32 gradient all-reduce
+(SURVEY §8d C4 row).
 
 Also measured in the same run:
   * replicated N-copy causal attention (same kernels, N(P+R) layout) and
-    the speedup vs it;
+    the speedup vs it (+ FA2 2.8.3 and torch varlen_attn on that layout);
   * e2e: the same step through the public API with pinned HOST buffers,
     H2D of every input and D2H of every output inside the timed region;
   * roofline of the dominant kernel, timed with CUDA events recorded by
@@ -26,9 +36,9 @@ bounded sample of the same workload and prints the same JSON line.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -39,7 +49,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "DualKV attn fwd+bwd ms & TFLOP/s at Qwen3-8B shapes N=32,P=8K; speedup vs N-copy"
-C3 = dict(n=32, p=8192, r=2048, h=32, hk=8, d=128)
 # BASELINE.json configs.  groups: prompt groups per GPU (weak) or in total (strong)
 CONFIGS = {
     "C1": dict(n=4, p=256, r=128, h=8, hk=8, d=64, dtype="f32", groups=1, scaling="weak",
@@ -49,17 +58,21 @@ CONFIGS = {
     "C3": dict(n=32, p=8192, r=2048, h=32, hk=8, d=128, dtype="bf16", groups=1, scaling="weak",
                desc="C3: Qwen3-8B attention, one prompt group N=32 P=8K R=2K per GPU"),
     "C4": dict(n=16, p=8192, r="ragged", h=32, hk=8, d=128, dtype="bf16", groups=64, scaling="strong",
-               desc="C4: 64 DAPO groups N=16 P=8K R_i~U[512,4096] (rng seed = group), LPT over GPUs"),
+               layer=True, d_model=4096, mb_groups=8,
+               desc="C4: 64 DAPO groups N=16 P=8K R_i~U[512,4096] (rng seed = group), LPT over GPUs; step = "
+                    "attention layer (repack + QKV proj + q/k RMSNorm + RoPE + two-call op + O proj, fwd+bwd) "
+                    "+ overlapped fp32 gradient all-reduce"),
     "C5": dict(n=32, p=16384, r=2048, h=32, hk=4, d=128, dtype="bf16", groups=8, scaling="weak",
-               desc="C5: Qwen3-30B-A3B attention (32/4 heads) N=32 P=16K R=2K, 8 groups per GPU"),
+               desc="C5: Qwen3-30B-A3B attention (32/4 heads) N=32 P=16K R=2K, 8 groups per GPU in one launch"),
 }
+# the CPU sample: full heads, a full C2-size prompt, one full response (bounded: ~7e11 FLOP/step)
+CPU_SAMPLE = dict(n=1, p=4096, r=1024, h=32, hk=8, d=128)
 
 
 def group_r_list(cfg, gidx):
     if cfg["r"] == "ragged":
         return [int(x) for x in np.random.default_rng(gidx).integers(512, 4097, cfg["n"])]
     return [cfg["r"]] * cfg["n"]
-CPU_SAMPLE = dict(n=4, p=2048, r=512, h=32, hk=8, d=128)  # same head config, fewer tokens
 
 
 def pairs(p, r_list):
@@ -69,11 +82,6 @@ def pairs(p, r_list):
 
 def flops_fwdbwd(cfg):
     return 14 * pairs(cfg["p"], [cfg["r"]] * cfg["n"]) * cfg["h"] * cfg["d"]
-
-
-def rep_flops_fwdbwd(cfg):
-    tri = lambda s: s * (s + 1) // 2
-    return 14 * cfg["n"] * tri(cfg["p"] + cfg["r"]) * cfg["h"] * cfg["d"]
 
 
 # ---------------------------------------------------------------- CPU side
@@ -144,11 +152,22 @@ def sample_desc():
             f"({flops_fwdbwd(c) / 1e9:.1f} GFLOP/step)")
 
 
+def cpu_full_c3():
+    """The one-off full-size C3 run of the same CPU path (tools/cpu_full_c3.py on a GPU box host),
+    committed under profiles/: the size-scaling caveat of the bounded sample, measured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_cpu_full_c3.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     tflops, sec = cpu_sample_tflops(reps=max(1, args.steps), warmup=args.warmup)
+    full = cpu_full_c3()
     line = {
         "metric": METRIC, "impl": "reference", "value": round(tflops, 6), "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -156,7 +175,8 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "C3 head shapes (H=32, Hk=8, d=128), bounded token sample", **CPU_SAMPLE},
         "cpu_baseline": {"value": round(tflops, 6), "unit": "TFLOP/s", "cores": cpu_threads(),
-                         "kind": "port", "sample": sample_desc(), "host": cpu_host()},
+                         "kind": "port", "sample": sample_desc(), "host": cpu_host(),
+                         "full_c3_measured": full},
         "e2e": {"value": round(tflops, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -229,6 +249,25 @@ class ClockSampler:
                 "window": "NVML polled every ~5 ms during the timed regions (main steps, fwd/bwd split)"}
 
 
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def _traffic():
+    """DRAM bytes per launch of the main kernels from the committed ncu --set full captures."""
+    for name in ("r2_traffic.json", "r1_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                return json.load(f), f"profiles/{name}"
+        except Exception:
+            continue
+    return {}, None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -280,28 +319,11 @@ def main():
         job_r = None  # every rank the same work
     pairs_rank = sum(visible_pairs(p, rl, "dualkv") for rl in my_r)
     fl_rank = 14 * pairs_rank * h * d
-    if job_r is not None:
-        fl_job = 14 * sum(visible_pairs(p, rl, "dualkv") for rl in job_r) * h * d
-    else:
-        fl_job = fl_rank * world
+    fl_job = 14 * sum(visible_pairs(p, rl, "dualkv") for rl in job_r) * h * d if job_r is not None \
+        else fl_rank * world
 
-    # buffers sized for the largest group; each group views a prefix (work depends on shape only)
-    tmax = max(sum(rl) for rl in my_r) if my_r else 0
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     mk = lambda *s_: torch.randn(*s_, device=dev, generator=g, dtype=torch.float32).to(dt)
-    qc, kc, vc, doc = mk(p, h, d), mk(p, hk, d), mk(p, hk, d), mk(p, h, d)
-    qb, kb, vb, dob = mk(tmax, h, d), mk(tmax, hk, d), mk(tmax, hk, d), mk(tmax, h, d)
-    groups = []
-    for rl in my_r:
-        t = sum(rl)
-        cu = np.concatenate([[0], np.cumsum(rl)]).astype(np.int64)
-        groups.append((dkv.DualKVInput(qb[:t], kc, vc, kb[:t], vb[:t], cu), dob[:t]))
-
-    def step():
-        # per group: Call 1 + Call 2 fused -- one forward launch, one backward launch
-        for dec, dod in groups:
-            oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc, dec)
-            dkv.dualkv_two_call_bwd(qc, dec, oc, lc, doc, od, ld, dod, deterministic=False)
 
     def barrier():
         if world > 1:
@@ -323,7 +345,39 @@ def main():
             ms_ = tt.item()
         return ms_
 
+    def kernel_events():
+        fms, fl, bms, bl, al = (ctypes.c_double(), ctypes.c_int32(), ctypes.c_double(), ctypes.c_int32(),
+                                ctypes.c_int32())
+        lib.dkv_profile_end(ctypes.byref(fms), ctypes.byref(fl), ctypes.byref(bms), ctypes.byref(bl),
+                            ctypes.byref(al))
+        return fms.value, fl.value, bms.value, bl.value, al.value
+
     clocks = ClockSampler()
+    peaks = _peaks()
+    peak_burst = peaks.get("bf16_tflops", 1590.0)
+    peak_sus = peaks.get("bf16_tflops_sustained", 1400.0)
+
+    if cfg.get("layer"):
+        return run_layer(args, cfg, dkv, torch, dist, world, rank, dev, my_r, fl_job, timed, barrier, clocks,
+                         kernel_events, peak_burst, peak_sus)
+
+    # ---- every group of this rank in ONE two-call launch (group table; one group = no table)
+    n_grp = len(my_r)
+    lens = [r for rl in my_r for r in rl]
+    t_all = sum(lens)
+    qc, kc, vc, doc = mk(n_grp * p, h, d), mk(n_grp * p, hk, d), mk(n_grp * p, hk, d), mk(n_grp * p, h, d)
+    qb, kb, vb, dob = mk(t_all, h, d), mk(t_all, hk, d), mk(t_all, hk, d), mk(t_all, h, d)
+    cu_all = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    table = {}
+    if n_grp > 1:
+        table = dict(group_seq_cu=np.concatenate([[0], np.cumsum([len(rl) for rl in my_r])]),
+                     group_ctx_cu=np.arange(0, n_grp * p + 1, p))
+    inp = dkv.DualKVInput(qb, kc, vc, kb, vb, cu_all, **table)
+
+    def step():
+        oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc, inp)
+        dkv.dualkv_two_call_bwd(qc, inp, oc, lc, doc, od, ld, dob, deterministic=False)
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -331,44 +385,48 @@ def main():
     # ---- headline: device-resident inputs, K steps, per-kernel CUDA events recorded by libdkv
     lib.dkv_profile_begin()
     ms = timed(step, args.steps)
-    fms, fl, bms, bl, al = (ctypes.c_double(), ctypes.c_int32(), ctypes.c_double(), ctypes.c_int32(),
-                            ctypes.c_int32())
-    lib.dkv_profile_end(ctypes.byref(fms), ctypes.byref(fl), ctypes.byref(bms), ctypes.byref(bl),
-                        ctypes.byref(al))
+    fms, fl, bms, bl, al = kernel_events()
     value = fl_job / (ms * 1e-3) / 1e12
 
-    # ---- first group: fwd / bwd split, separate-call comparison, replicated N-copy baseline, e2e
-    dec0, dod0 = groups[0]
-    rl0 = my_r[0]
-    pairs0 = visible_pairs(p, rl0, "dualkv")
+    # ---- fwd / bwd split of the same launches
     saved = {}
 
     def fwd_only():
-        saved["oc"], saved["lc"], saved["od"], saved["ld"] = dkv.dualkv_two_call_fwd(qc, dec0)
+        saved["oc"], saved["lc"], saved["od"], saved["ld"] = dkv.dualkv_two_call_fwd(qc, inp)
 
     for _ in range(2):  # warm the allocator for this call pattern (two live output sets) before timing it
         fwd_only()
     fwd_ms = timed(fwd_only, args.steps)
 
     def bwd_only():
-        dkv.dualkv_two_call_bwd(qc, dec0, saved["oc"], saved["lc"], doc, saved["od"], saved["ld"], dod0,
+        dkv.dualkv_two_call_bwd(qc, inp, saved["oc"], saved["lc"], doc, saved["od"], saved["ld"], dob,
                                 deterministic=False)
 
     for _ in range(2):
         bwd_only()
     bwd_ms = timed(bwd_only, args.steps)
     clocks.pause()
-    ctx_b = dkv.VarlenBatch(qc, kc, vc, np.array([0, p]))
+
+    # ---- group 0 alone: the reference's two separate calls, the replicated N-copy baseline, e2e
+    rl0 = my_r[0]
+    t0 = sum(rl0)
+    pairs0 = visible_pairs(p, rl0, "dualkv")
+    cu0 = np.concatenate([[0], np.cumsum(rl0)]).astype(np.int64)
+    qc0, kc0, vc0, doc0 = qc[:p], kc[:p], vc[:p], doc[:p]
+    dec0 = dkv.DualKVInput(qb[:t0], kc0, vc0, kb[:t0], vb[:t0], cu0)
+    dod0 = dob[:t0]
+    ctx_b = dkv.VarlenBatch(qc0, kc0, vc0, np.array([0, p]))
 
     def step_separate():
         # the reference's two separate calls (layer.py:243-255, 274-275), for comparison
         oc, lc = dkv.fa2_varlen_fwd(ctx_b)
         od, ld = dkv.dualkv_fwd(dec0)
         dkv.dualkv_bwd(dec0, od, ld, dod0, deterministic=False)
-        dkv.fa2_varlen_bwd(ctx_b, oc, lc, doc)
+        dkv.fa2_varlen_bwd(ctx_b, oc, lc, doc0)
 
     step_separate()
     sep_ms = timed(step_separate, args.steps)
+    grp_ms = ms / n_grp  # the headline step (fwd+bwd of Call 1 + Call 2) per group
 
     rep = None
     if not args.no_replicated:
@@ -382,12 +440,17 @@ def main():
             dkv.fa2_varlen_bwd(rb, o, l_, dor)
 
         rep_step()
+        lib.dkv_profile_begin()
         rep_ms = timed(rep_step, max(1, min(args.steps, 3)))
-        grp_ms = ms / max(1, len(my_r))  # the headline step (fwd+bwd of Call 1 + Call 2) per group
-        # the same replicated problem through a library kernel, for scale: FlashAttention-2
+        rfms, _, rbms, _, _ = kernel_events()
+        rep_steps = max(1, min(args.steps, 3))
+        rep_pairs = visible_pairs(p, rl0, "standard")
+        # the same replicated problem through library kernels, for scale: FlashAttention-2
         # (flash_attn 2.8.3, mma.sync SASS for sm_100) varlen causal fwd+bwd
         ext = None
         try:
+            if dt != torch.bfloat16:
+                raise RuntimeError("skipped: FA2 has no fp32 path")
             if qr.numel() >= 2 ** 31:
                 # FA2 2.8.3 faults (illegal address) past 2^31 query elements; skip rather than
                 # poison the CUDA context for the rest of the run
@@ -405,7 +468,7 @@ def main():
             fa2_ms = timed(fa2_step, max(1, min(args.steps, 3)))
             ext = {"impl": "flash_attn 2.8.3 flash_attn_varlen_func (FA2, sm_100 build)",
                    "ms_per_group": round(fa2_ms, 3),
-                   "speedup_dualkv_vs_fa2_ncopy": round(fa2_ms / (ms / max(1, len(my_r))), 3)}
+                   "speedup_dualkv_vs_fa2_ncopy": round(fa2_ms / grp_ms, 3)}
             del qx, kx, vx
         except Exception as exc:  # library missing / unsupported on this build
             ext = {"unavailable": str(exc)[:120]}
@@ -413,6 +476,8 @@ def main():
         # window (-1, 0); K/V expanded to the H query heads -- it takes one head count)
         tv = None
         try:
+            if dt != torch.bfloat16:
+                raise RuntimeError("skipped: bf16 only")
             if qr.numel() >= 2 ** 31:
                 raise RuntimeError("skipped past 2^31 query elements")
             from torch.nn.attention.varlen import varlen_attn
@@ -431,15 +496,23 @@ def main():
             tv_ms = timed(tv_step, max(1, min(args.steps, 3)))
             tv = {"impl": "torch.nn.attention.varlen.varlen_attn (torch " + torch.__version__ + ")",
                   "ms_per_group": round(tv_ms, 3),
-                  "speedup_dualkv_vs_torch_varlen_ncopy": round(tv_ms / (ms / max(1, len(my_r))), 3)}
+                  "speedup_dualkv_vs_torch_varlen_ncopy": round(tv_ms / grp_ms, 3)}
             del qx, kx, vx
         except Exception as exc:
             tv = {"unavailable": str(exc)[:120]}
+        rep_tf = 14 * rep_pairs * h * d / (rep_ms * 1e-3) / 1e12
+        rep_kernel_tf = 14 * rep_pairs * h * d * rep_steps / ((rfms + rbms) * 1e-3) / 1e12 if rfms + rbms else None
+        dk_kernel_tf = fl_rank * args.steps / ((fms + bms) * 1e-3) / 1e12 if fms + bms else None
         rep = {"ms_per_group": round(rep_ms, 3), "library_baseline": ext, "torch_varlen_baseline": tv,
-               "tflops_algorithmic": round(14 * visible_pairs(p, rl0, "standard") * h * d / (rep_ms * 1e-3) / 1e12, 2),
+               "tflops_algorithmic": round(rep_tf, 2),
+               "kernel_tflops": round(rep_kernel_tf, 2) if rep_kernel_tf else None,
                "dualkv_ms_per_group": round(grp_ms, 3),
                "speedup_dualkv_vs_ncopy": round(rep_ms / grp_ms, 3),
-               "pair_ratio": round(visible_pairs(p, rl0, "standard") / pairs0, 3)}
+               "pair_ratio": round(rep_pairs / pairs0, 3),
+               # per-FLOP efficiency of the two paths' main kernels (1.0: the N-copy saving is all
+               # from the avoided work, none from kernel efficiency differences)
+               "efficiency_ratio_dualkv_over_ncopy": round(dk_kernel_tf / rep_kernel_tf, 3)
+               if dk_kernel_tf and rep_kernel_tf else None}
         del qr, kr, vr, dor, rb
 
     # ---- the step before attention: repack N(P+R) -> P+NR fused with RoPE at
@@ -453,25 +526,18 @@ def main():
             dkv.repack_rope_to_dualkv(*xs, plan, 1e6)
         rp_ms = timed(lambda: dkv.repack_rope_to_dualkv(*xs, plan, 1e6), args.steps)
         moved = 2 * plan.total_dualkv * (h + 2 * hk) * d * 2  # gathered rows read + written once
-        hbm = peaks_hbm = None
-        try:
-            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-                peaks_hbm = json.load(f).get("hbm_gbs")
-        except Exception:
-            pass
         gbs = moved / (rp_ms * 1e-3) / 1e9
+        hbm = peaks.get("hbm_gbs")
         repack = {"ms": round(rp_ms, 4), "bytes": moved, "GB_per_s": round(gbs, 1),
-                  "frac_of_hbm": round(gbs / peaks_hbm, 3) if peaks_hbm else None,
+                  "frac_of_hbm": round(gbs / hbm, 3) if hbm else None,
                   "what": "repack_rope_to_dualkv: q,k,v gathered from the replicated layout, q,k rotated at "
                           "logical positions (prompt j -> j, response r -> P + r), one group"}
         del xs
 
     e2e = None
     if not args.no_e2e:
-        t0 = sum(rl0)
-        cu0 = np.concatenate([[0], np.cumsum(rl0)]).astype(np.int64)
         host_in = {k: v.cpu().pin_memory() for k, v in
-                   dict(qc=qc, kc=kc, vc=vc, q=qb[:t0], kd=kb[:t0], vd=vb[:t0], doc=doc, dod=dob[:t0]).items()}
+                   dict(qc=qc0, kc=kc0, vc=vc0, q=qb[:t0], kd=kb[:t0], vd=vb[:t0], doc=doc0, dod=dod0).items()}
         out_shapes = [(p, h, d), (t0, h, d), (t0, h, d), (p, hk, d), (p, hk, d), (t0, hk, d), (t0, hk, d),
                       (p, h, d)]
         host_out = [[torch.empty(s_, dtype=dt).pin_memory() for s_ in out_shapes] for _ in range(2)]
@@ -559,27 +625,13 @@ def main():
     clk = clocks.stop()
 
     # ---- roofline of the dominant kernel (the backward main kernel)
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except Exception:
-        pass
-    peak_burst = peaks.get("bf16_tflops", 1590.0)
-    peak_sus = peaks.get("bf16_tflops_sustained", 1400.0)
-    # DRAM traffic of the same kernels from the committed ncu --set full capture (per launch)
-    traffic = {}
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-            traffic = json.load(f)
-    except Exception:
-        pass
+    traffic, traffic_src = _traffic()
     tb = traffic.get("dualkv_bwd_kernel", {})
     tf = traffic.get("dualkv_fwd_kernel<128>", {})
-    # per step and group each main kernel launches once (Call 1 fused into Call 2's launch):
+    # per step each main kernel launches once (all groups, Call 1 fused into Call 2's launch):
     # achieved = algorithmic FLOPs of those launches / their device time (CUDA events by libdkv)
-    bwd_ach = 10 * pairs_rank * h * d * args.steps / (bms.value * 1e-3) / 1e12 if bms.value else 0.0
-    fwd_ach = 4 * pairs_rank * h * d * args.steps / (fms.value * 1e-3) / 1e12 if fms.value else 0.0
+    bwd_ach = 10 * pairs_rank * h * d * args.steps / (bms * 1e-3) / 1e12 if bms else 0.0
+    fwd_ach = 4 * pairs_rank * h * d * args.steps / (fms * 1e-3) / 1e12 if fms else 0.0
     roof = {"bound": "tensor", "kernel": "dualkv_bwd_kernel (tcgen05; Call 1 fused into the Call 2 launch)",
             "achieved": round(bwd_ach, 2), "peak": peak_sus, "unit": "TFLOP/s",
             "frac": round(bwd_ach / peak_sus, 4),
@@ -587,24 +639,24 @@ def main():
             "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (the kernel runs inside a multi-step loop "
                             "under sw_power_cap); frac_of_burst uses bf16_tflops") if peaks else "fallback",
             "frac_of_burst": round(bwd_ach / peak_burst, 4), "peak_burst": peak_burst,
-            "traffic_source": "profiles/r1_traffic.json (ncu --set full, dram__bytes_read+write, one C3 launch)",
+            "traffic_source": f"{traffic_src} (ncu --set full, dram__bytes_read+write, one C3 launch)",
             "algorithmic_per_launch": "10 * visible_pairs * H * d FLOP (SURVEY 8d); "
-                                      f"{10 * pairs0 * h * d:.4e} per group",
+                                      f"{10 * pairs_rank * h * d:.4e} per launch ({n_grp} group(s))",
             "fwd_kernel": {"achieved": round(fwd_ach, 2), "frac": round(fwd_ach / peak_sus, 4),
                            "frac_of_burst": round(fwd_ach / peak_burst, 4),
                            "traffic": (tf["dram_read_bytes"] + tf["dram_write_bytes"]) if tf else None},
-            "kernel_ms": {"fwd_main_per_launch": round(fms.value / max(1, fl.value), 4),
-                          "bwd_main_per_launch": round(bms.value / max(1, bl.value), 4),
-                          "fwd_main_share": round(fms.value / (ms * args.steps), 3),
-                          "bwd_main_share": round(bms.value / (ms * args.steps), 3)}}
+            "kernel_ms": {"fwd_main_per_launch": round(fms / max(1, fl), 4),
+                          "bwd_main_per_launch": round(bms / max(1, bl), 4),
+                          "fwd_main_share": round(fms / (ms * args.steps), 3),
+                          "bwd_main_share": round(bms / (ms * args.steps), 3)}}
     step_frac = {"of_sustained": round(value / max(1, world) / peak_sus, 4),
                  "of_burst": round(value / max(1, world) / peak_burst, 4)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        tf, sec = cpu_sample_tflops(reps=1, warmup=0)
-        cpu = {"value": round(tf, 6), "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port", "host": cpu_host(),
-               "sample": sample_desc(), "seconds": round(sec, 2)}
+        tf_, sec = cpu_sample_tflops(reps=1, warmup=0)
+        cpu = {"value": round(tf_, 6), "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port", "host": cpu_host(),
+               "sample": sample_desc(), "seconds": round(sec, 2), "full_c3_measured": cpu_full_c3()}
 
     if rank == 0:
         line = {
@@ -614,18 +666,98 @@ def main():
             "dtype": cfg["dtype"], "data": "synthetic (randn)",
             "config": {"workload": cfg["desc"], "N": cfg["n"], "P": p,
                        "R": cfg["r"] if cfg["r"] != "ragged" else "U[512,4096]",
-                       "H": h, "H_k": hk, "d": d, "groups_this_rank": len(my_r),
+                       "H": h, "H_k": hk, "d": d, "groups_this_rank": n_grp,
+                       "launches": "one fwd + one bwd launch for all groups of the rank (group table)",
                        "parallelism": f"dp{world} over prompt groups",
-                       "l2": "inputs larger than L2" if tmax * h * d * 2 > 126e6 else "inputs may fit in L2",
+                       "l2": "inputs larger than L2" if t_all * h * d * 2 > 126e6 else "inputs may fit in L2",
                        "unit_of_work": "Call1+Call2 fwd+bwd (reference run_bench dk unit), fused two-call launches",
                        "flops_per_step_job": fl_job},
-            "fwd_ms_group0": round(fwd_ms, 3), "bwd_ms_group0": round(bwd_ms, 3),
-            "fwd_tflops": round(4 * pairs0 * h * d / (fwd_ms * 1e-3) / 1e12, 2),
-            "bwd_tflops": round(10 * pairs0 * h * d / (bwd_ms * 1e-3) / 1e12, 2),
+            "us_per_step": round(ms * 1e3, 1),
+            "fwd_ms": round(fwd_ms, 3), "bwd_ms": round(bwd_ms, 3),
+            "fwd_tflops": round(4 * pairs_rank * h * d / (fwd_ms * 1e-3) / 1e12, 2),
+            "bwd_tflops": round(10 * pairs_rank * h * d / (bwd_ms * 1e-3) / 1e12, 2),
             "separate_calls_ms_group0": round(sep_ms, 3),
             "step_frac_of_peak": step_frac,
             "replicated_ncopy": rep, "repack_rope": repack, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
-            "gpu_launches": int(al.value), "clocks": clk,
+            "gpu_launches": int(al), "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_layer(args, cfg, dkv, torch, dist, world, rank, dev, my_r, fl_job, timed, barrier, clocks, kernel_events,
+              peak_burst, peak_sus):
+    """C4: the attention layer step over this rank's groups in micro-batches of `mb_groups` groups
+    (one multi-group launch each), gradient accumulation, overlapped fp32 gradient all-reduce."""
+    from paper_2605_15422_b200 import packing as pk
+    from paper_2605_15422_b200._lib import lib
+    from paper_2605_15422_b200.costmodel import visible_pairs
+    from paper_2605_15422_b200.dp import GradSync
+    from paper_2605_15422_b200.layer import DualKVBatch, DualKVSelfAttention
+
+    p, h, hk, d, dm = cfg["p"], cfg["h"], cfg["hk"], cfg["d"], cfg["d_model"]
+    torch.manual_seed(0)
+    blk = DualKVSelfAttention(dm, h, hk, d, rope_base=1e6, qk_norm=True, device=dev)
+    sync = GradSync(list(blk.parameters()), overlap=True)
+    mbs = []
+    for i in range(0, len(my_r), cfg["mb_groups"]):
+        plan = pk.make_plan([(p, rl) for rl in my_r[i:i + cfg["mb_groups"]]])
+        mbs.append((plan, DualKVBatch.from_plan(plan, dev)))
+    t_std = max((m[0].total_standard for m in mbs), default=0)
+    t_dk = max((m[0].total_dualkv for m in mbs), default=0)
+    g = torch.Generator(device=dev).manual_seed(77 + rank)
+    x_std = (torch.randn(t_std, dm, device=dev, generator=g) * 0.5).to(torch.bfloat16)
+    dy = torch.randn(t_dk, dm, device=dev, generator=g).to(torch.bfloat16)
+
+    def step():
+        for i, (plan, batch) in enumerate(mbs):
+            x = pk.repack_to_dualkv(x_std[:plan.total_standard], plan)  # the device repack of the inputs
+            ctx = sync.no_sync() if i < len(mbs) - 1 else contextlib.nullcontext()
+            with ctx:
+                blk(x, batch).backward(dy[:plan.total_dualkv])
+        sync.sync()
+        blk.zero_grad(set_to_none=True)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks.start()
+    lib.dkv_profile_begin()
+    ms = timed(step, args.steps)
+    fms, fl, bms, bl, al = kernel_events()
+    clk = clocks.stop()
+    value = fl_job / (ms * 1e-3) / 1e12
+    rows = sum(m[0].total_dualkv for m in mbs)
+    proj_fl_rank = 3 * 2 * rows * dm * (h + 2 * hk) * d + 3 * 2 * rows * h * d * dm  # QKV + O proj, fwd+bwd
+    fl_attn_rank = 14 * sum(visible_pairs(p, rl, "dualkv") for rl in my_r) * h * d
+    attn_ms = (fms + bms) / max(1, args.steps)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (randn hidden states, random-init layer weights)",
+            "value_definition": "attention algorithmic FLOPs of all 64 groups (14*pairs*H*d) / layer-step time: "
+                                "the projection GEMMs, norms, RoPE, repack and all-reduce are inside the step "
+                                "but not counted",
+            "config": {"workload": cfg["desc"], "N": cfg["n"], "P": p, "R": "U[512,4096]", "H": h, "H_k": hk,
+                       "d": d, "d_model": dm, "groups_job": cfg["groups"], "groups_this_rank": len(my_r),
+                       "micro_batches_this_rank": len(mbs), "groups_per_micro_batch": cfg["mb_groups"],
+                       "parallelism": f"dp{world} over prompt groups (LPT on visible pairs)",
+                       "l2": "inputs larger than L2", "flops_per_step_job": fl_job},
+            "groups_per_s": round(cfg["groups"] / (ms * 1e-3), 3),
+            "layer_tflops_rank0": round((fl_attn_rank + proj_fl_rank) / (ms * 1e-3) / 1e12, 2),
+            "attention_kernels_ms_per_step_rank0": round(attn_ms, 3),
+            "attention_kernel_tflops_rank0": round(fl_attn_rank / (attn_ms * 1e-3) / 1e12, 2) if attn_ms else None,
+            "attention_share_of_step": round(attn_ms / ms, 3),
+            "roofline": {"bound": "tensor", "kernel": "dualkv_bwd_kernel (multi-group launch)",
+                         "achieved": round(10 * fl_attn_rank / 14 * args.steps / (bms * 1e-3) / 1e12, 2)
+                         if bms else None, "peak": peak_sus, "unit": "TFLOP/s",
+                         "frac": round(10 * fl_attn_rank / 14 * args.steps / (bms * 1e-3) / 1e12 / peak_sus, 4)
+                         if bms else None, "traffic": None},
+            "e2e": None, "cpu_baseline": None, "gpu_launches": int(al), "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

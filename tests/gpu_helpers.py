@@ -91,17 +91,20 @@ def ref_attention_slice_f64(q, keys, vals, d_out, offset, scale, block=2048):
     return torch.cat(o_all), torch.cat(lse_all, dim=1), torch.cat(dq_all), dk, dv
 
 
-def assert_bf16_vs_f64(got, ref, what, max_rel=1e-2):
+def assert_bf16_vs_f64(got, ref, what, max_rel=1e-2, elementwise=True):
     """SURVEY §8c bf16 bounds against the f64 reference: elementwise |gpu-ref| <= 1e-2 + 1e-2|ref|,
     and max|gpu - ref| / max|ref| <= 1e-2 (the scale-aware bound; the elementwise one alone is loose
-    for gradients much smaller than 1)."""
+    for gradients much smaller than 1).  `elementwise=False` (sums over ~10^5-10^6 bf16-operand
+    terms, checked with the FA-style comparative bound instead) keeps only the max-relative one.
+    Returns (max-relative error, fraction of elements outside the elementwise bound)."""
     g = got.double()
     r = ref.double()
     assert g.shape == r.shape, (what, tuple(g.shape), tuple(r.shape))
     assert torch.isfinite(g).all(), f"{what}: non-finite values"
     err = (g - r).abs()
     bad = err > BF16_ATOL + BF16_RTOL * r.abs()
-    assert not bad.any(), f"{what}: {int(bad.sum())} elements outside 1e-2 + 1e-2|ref| (max err {err.max():.3e})"
+    if elementwise:
+        assert not bad.any(), f"{what}: {int(bad.sum())} elements outside 1e-2 + 1e-2|ref| (max err {err.max():.3e})"
     rel = (err.max() / r.abs().max().clamp_min(1e-300)).item()
     assert rel <= max_rel, f"{what}: max err / max|ref| = {rel:.3e} > {max_rel}"
-    return rel
+    return rel, bad.double().mean().item()
