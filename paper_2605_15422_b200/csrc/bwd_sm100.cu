@@ -53,6 +53,12 @@ constexpr int kDrainT0 = kWDrain * 32;  // first drain thread
 #define BWD_POLY 0  // sweep 0/2/4/6: 27.5/27.7/28.1/27.9 ms (noise-level; MUFU is not the limit here)
 #endif
 constexpr int kPolyPairs = BWD_POLY;    // of every 16 exponential pairs, on the FMA pipe
+#ifndef BWD_OWN_ORDER
+// own-response items: 0 kv head fastest, then sequence, then key tile; 1 key tile fastest within
+// (sequence, kv head).  A/B at C3 (profiles/r2_ab.md): 1 is 1.5x faster on the causal N-copy
+// backward (108 -> 71 ms) and 5 % on the DualKV backward (its own-response items)
+#define BWD_OWN_ORDER 1
+#endif
 constexpr int kStages = 3;
 constexpr int kKVPanel = kBK * 128;         // 16 KB: one 64-column SW128 panel of a key tile
 constexpr int kPBytes = kBK * kBQ * 2;      // 16 KB
@@ -94,6 +100,7 @@ struct Params {
   const int32_t* cu;
   int num_seqs, total_q, ctx_len, heads, kv_heads, group, tq, tpad;
   int chunk, max_chunks, n_ctx_items, n_ctx_tiles;  // n_ctx_tiles: of the longest group prompt
+  int max_own_tiles;                               // key tiles of the longest response
   int atomic_ctx;
   int ablate;  // timing experiments only (DKV_BWD_ABLATE): 1 drain I/O, 2 compute math, 4 Q/dO loads,
                // 8 the additive-constant MMAs
@@ -184,10 +191,19 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
   } else if (bid >= p.n_ctx_items + p.n_self_items) {
     kind = 1;
     const int b2 = bid - p.n_ctx_items - p.n_self_items;
+#if BWD_OWN_ORDER == 1
+    // a (sequence, kv head)'s key tiles side by side: co-resident CTAs stream the same Q / dO /
+    // (lse, D) rows and reduce into the same dQ accumulator lines in L2
+    ktile = b2 % p.max_own_tiles;
+    const int r2 = b2 / p.max_own_tiles;
+    hk = r2 % p.kv_heads;
+    s0 = r2 / p.kv_heads;
+#else
     hk = b2 % p.kv_heads;
     const int r2 = b2 / p.kv_heads;
     s0 = r2 % p.num_seqs;
     ktile = r2 / p.num_seqs;
+#endif
     s1 = s0 + 1;
     kv_len = p.cu[s0 + 1] - p.cu[s0];
     if (ktile * kBK >= kv_len) return;
@@ -646,6 +662,7 @@ static int launch(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp,
   p.scale = a.scale;
   p.scale_log2 = a.scale * 1.4426950408889634f;
   const int max_tiles = a.total_q > 0 ? (a.max_seqlen + kBK - 1) / kBK : 0;
+  p.max_own_tiles = std::max(1, max_tiles);
   const int64_t grid = static_cast<int64_t>(p.n_ctx_items) + p.n_self_items +
                        static_cast<int64_t>(max_tiles) * a.num_seqs * a.kv_heads;
   if (grid == 0) return DKV_OK;

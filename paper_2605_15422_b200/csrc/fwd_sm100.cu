@@ -42,6 +42,16 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define FWD_POLY 5
 #endif
 constexpr int kPolyPairs = FWD_POLY;       // of every 16 exponential pairs, on the FMA pipe
+#ifndef FWD_EVICT
+// L2 hint of the own-region K/V tiles: 0 evict_last (as the prompt's), 1 normal, 2 first
+#define FWD_EVICT 1
+#endif
+#ifndef FWD_ORDER
+// main work-item order: 0 kv head fastest, then sequence, then q block; 1 q block fastest within
+// (sequence, kv head).  A/B at C3 (tools/ab.sh, profiles/r2_ab.md): 1 + evict-normal own K/V is
+// 3 % faster for the DualKV forward and 1.3x for the causal (N-copy / Call 1) forward
+#define FWD_ORDER 1
+#endif
 
 template <int D>
 struct Cfg {
@@ -71,6 +81,7 @@ struct Params {
   const int32_t* cu;
   int num_seqs, total_q, ctx_len, heads, kv_heads, group, tq;
   int n_main_items;       // items >= n_main_items are Call 1 items (causal self-attention over the prompt)
+  int blocks_per_seq;     // q blocks (items) per (sequence, kv head) of the longest sequence
   float scale_log2;       // softmax_scale * log2(e)
   int ablate;             // timing experiments only (DKV_FWD_ABLATE): 1 K/V loads, 2 exponentials
   GroupTable grp;         // prompt groups of the launch (one group: {0, num_seqs} / {0, ctx_len})
@@ -118,10 +129,18 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
   __nv_bfloat16* out;
   float* lse_out;
   if (!self_item) {
+#if FWD_ORDER == 1
+    // a (sequence, kv head)'s q blocks side by side: co-resident CTAs share its own K/V stream in L2
+    jb = item % p.blocks_per_seq;
+    const int rest = item / p.blocks_per_seq;
+    hk = rest % p.kv_heads;
+    const int seq = rest / p.kv_heads;
+#else
     hk = item % p.kv_heads;
     const int rest = item / p.kv_heads;
     const int seq = rest % p.num_seqs;
     jb = rest / p.num_seqs;
+#endif
     seq0 = p.cu[seq];
     rlen = p.cu[seq + 1] - seq0;
     const int g = p.grp.group_of(seq);
@@ -224,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         tma_prefetch(&p.tm_vc);
       }
       const uint64_t pol_kv = policy_evict_last();
+      const uint64_t pol_own = FWD_EVICT == 1 ? policy_evict_normal() : policy_evict_first();
       if constexpr (kPair) {
         if (crank == 0) mbar_arrive_expect_tx(&sm.q_full, 4 * C::kTileBytes);
         const uint32_t lq = mapa_shared(&sm.q_full, 0);
@@ -264,15 +284,18 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
           continue;
         }
         const bool skip_kv = (DKV_ABL(p.ablate) & 1) || ((DKV_ABL(p.ablate) & 4) && it >= C::kStages);  // 4: reuse the first tiles
+        // L2 policy: the shared prompt's K/V is re-read by every sequence's items -> evict_last;
+        // a sequence's own K/V only by that sequence's few items (FWD_EVICT selects, see top)
+        const uint64_t pol = (is_ctx || FWD_EVICT == 0) ? pol_kv : pol_own;
         mbar_arrive_expect_tx(&sm.k_full[slot], skip_kv ? 0 : C::kTileBytes);
         for (int pn = 0; pn < C::kPanels && !skip_kv; ++pn)
           tma_load_3d_hint(sK + slot * C::kTileBytes + pn * C::kPanelBytes, mk, &sm.k_full[slot], pn * 64, hk,
-                           row, pol_kv);
+                           row, pol);
         mbar_wait(&sm.v_empty[slot], ph ^ 1);
         mbar_arrive_expect_tx(&sm.v_full[slot], skip_kv ? 0 : C::kTileBytes);
         for (int pn = 0; pn < C::kPanels && !skip_kv; ++pn)
           tma_load_3d_hint(sV + slot * C::kTileBytes + pn * C::kPanelBytes, mv, &sm.v_full[slot], pn * 64, hk,
-                           row, pol_kv);
+                           row, pol);
       }
     }
     __syncwarp();
@@ -608,6 +631,7 @@ int launch(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, cudaSt
     return DKV_ERR_UNSUPPORTED;
   }
   p.n_main_items = static_cast<int>(main_items);
+  p.blocks_per_seq = blocks_per_seq;
   if (pair) {
     const void* fn = reinterpret_cast<const void*>(dualkv_fwd_kernel<128, true>);
     if (!ensure_smem_optin(fn, C::kSmemBytesPair, "dualkv_fwd_kernel(pair)")) return DKV_ERR_CUDA;
