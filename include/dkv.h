@@ -189,6 +189,27 @@ DKV_API int32_t dkv_rope_qkv_rows(const void* q_src, const void* k_src, const vo
                                   int64_t kv_heads, int64_t head_dim, const int64_t* positions,
                                   const int64_t* idx, double base, int32_t inverse, void* stream);
 
+/* The step between the QKV projection and the DualKV op, one HBM pass (reference
+ * layer.py:182-205 for RoPE, packing.py:105-120 for positions; Qwen3's per-head q/k RMSNorm,
+ * SPEC.md:464, when the norm weights are given): for every packed row r of
+ * qkv [rows, heads + 2 kv_heads, head_dim] (bf16, the GEMM output):
+ *   q / k heads: y = RoPE(pos[r]) (x * rsqrt(mean(x^2) + eps) * w)   (fp32, rounded once)
+ *   v heads:     copied
+ * written at row dst_rows[r] of q [rows, heads, d], k / v [rows, kv_heads, d].  norm weights: bf16
+ * [head_dim] each, both NULL for no norm.  head_dim 64 / 128 / 256.  Device int64 arrays. */
+DKV_API int32_t dkv_qkv_prep_fwd(const void* qkv, const void* q_norm_w, const void* k_norm_w, float eps,
+                                 const int64_t* positions, const int64_t* dst_rows, void* q, void* k, void* v,
+                                 int64_t rows, int64_t heads, int64_t kv_heads, int64_t head_dim, double base,
+                                 void* stream);
+/* Its adjoint: dq / dk / dv (rows in the dst_rows layout) -> dqkv [rows, heads + 2 kv_heads, d] (packed
+ * order) and, with norm weights, their fp32 gradients dq_norm_w / dk_norm_w [head_dim] (zeroed and
+ * accumulated by the call).  qkv is the forward's input (the norm is recomputed from it). */
+DKV_API int32_t dkv_qkv_prep_bwd(const void* dq, const void* dk, const void* dv, const void* qkv,
+                                 const void* q_norm_w, const void* k_norm_w, float eps, const int64_t* positions,
+                                 const int64_t* dst_rows, void* dqkv, float* dq_norm_w, float* dk_norm_w,
+                                 int64_t rows, int64_t heads, int64_t kv_heads, int64_t head_dim, double base,
+                                 void* stream);
+
 /* Kernel timing for the bench harness: while enabled, the library records a
  * CUDA event pair (on the launching stream) around every main attention
  * kernel and counts every kernel it launches.  dkv_profile_end synchronises

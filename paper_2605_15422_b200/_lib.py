@@ -84,6 +84,10 @@ SIGNATURES = {
                                        ctypes.c_int32, _vp]),
     "dkv_rope_qkv_rows": (ctypes.c_int32, [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int32, _i64, _i64, _i64, _i64,
                                            _vp, _vp, ctypes.c_double, ctypes.c_int32, _vp]),
+    "dkv_qkv_prep_fwd": (ctypes.c_int32, [_vp, _vp, _vp, ctypes.c_float, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
+                                          _i64, ctypes.c_double, _vp]),
+    "dkv_qkv_prep_bwd": (ctypes.c_int32, [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_float, _vp, _vp, _vp, _vp, _vp,
+                                          _i64, _i64, _i64, _i64, ctypes.c_double, _vp]),
     "dkv_selftest_umma": (ctypes.c_int32, [ctypes.c_int32, _vp, _vp, _vp, _vp]),
     "dkv_profile_begin": (ctypes.c_int32, []),
     "dkv_profile_end": (ctypes.c_int32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32),

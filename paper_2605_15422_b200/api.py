@@ -329,7 +329,7 @@ def fa2_varlen_fwd(batch: VarlenBatch) -> Tuple[torch.Tensor, torch.Tensor]:
 # ---------------------------------------------------------------------------
 
 def _bwd_params(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse, d_out, deterministic,
-                ctx_chunk=0, groups=None):
+                ctx_chunk=0, groups=None, grads=None):
     """Shape checks (kernel.py:214-218), output allocation and the C parameter block of one backward."""
     t, h, d = q.shape
     for name, x in (("O", out), ("dO", d_out), ("lse", lse)):
@@ -342,9 +342,12 @@ def _bwd_params(q, kc, vc, k, v, cu_dev, n, p_len, grid_max, scale, out, lse, d_
         raise ValueError(f"lse shape {tuple(lse.shape)} != {(h, t)}")
     keep = dict(out=out.to(q.dtype).contiguous(), d_out=d_out.to(q.dtype).contiguous(),
                 lse=lse.to(torch.float32).contiguous())
-    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-    dkc = torch.empty_like(kc) if kc is not None else None
-    dvc = torch.empty_like(vc) if vc is not None else None
+    if grads is not None:  # caller-provided output views (dq, dk_ctx, dv_ctx, dk, dv)
+        dq, dkc, dvc, dk, dv = grads
+    else:
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        dkc = torch.empty_like(kc) if kc is not None else None
+        dvc = torch.empty_like(vc) if vc is not None else None
     prm = BwdParams()
     prm.q, prm.k_ctx, prm.v_ctx, prm.k, prm.v = _ptr(q), _ptr(kc), _ptr(vc), _ptr(k), _ptr(v)
     prm.cu_seqlens, prm.out = cu_dev.data_ptr(), _ptr(keep["out"])
@@ -594,3 +597,60 @@ def dualkv_two_call_attention(q_context, k_context, v_context, q_decoded, k_deco
     q_ctx = _check_prompt_q(q_context, inp)
     from . import library
     return library.two_call_attention(q_ctx, inp)
+
+
+# ---------------------------------------------------------------------------
+# the two-call op over ONE buffer per tensor: rows [0, P_total) are every group's prompt, the rest
+# every group's responses (the layer's split layout).  Outputs / gradients land in single buffers
+# of the same layout -- no concatenation or slice-gradient assembly around the op.
+# ---------------------------------------------------------------------------
+
+def _split_input(q, k, v, p_rows, cu_seqlens, max_seqlen, softmax_scale, group_seq_cu, group_ctx_cu):
+    return DualKVInput(q[p_rows:], k[:p_rows], v[:p_rows], k[p_rows:], v[p_rows:], cu_seqlens,
+                       max_seqlen_q=max_seqlen, softmax_scale=softmax_scale,
+                       group_seq_cu=group_seq_cu or None, group_ctx_cu=group_ctx_cu or None)
+
+
+def two_call_split_fwd(q, k, v, p_rows: int, cu_seqlens, max_seqlen: int, softmax_scale: float,
+                       group_seq_cu=None, group_ctx_cu=None):
+    """-> (O [T, H, d] in the same split layout, lse_ctx [H, P], lse [H, T - P])."""
+    inp = _split_input(q, k, v, p_rows, cu_seqlens, max_seqlen, softmax_scale, group_seq_cu, group_ctx_cu)
+    q_ctx = _check_prompt_q(q[:p_rows], inp)
+    t, h, d = q.shape
+    with torch.cuda.device(q.device):
+        out = torch.empty_like(q)
+        lse_c = torch.empty((h, p_rows), dtype=torch.float32, device=q.device)
+        lse = torch.empty((h, t - p_rows), dtype=torch.float32, device=q.device)
+        prm = TwoCallFwdParams()
+        prm.call2 = _fwd_params(inp.q, inp.k_context, inp.v_context, inp.k_decoded, inp.v_decoded, inp.cu_dev,
+                                inp.num_sequences, p_rows, inp._grid_max, inp.softmax_scale, out[p_rows:], lse,
+                                inp._groups)
+        prm.q_ctx, prm.out_ctx, prm.lse_ctx = _ptr(q_ctx), _ptr(out[:p_rows]), _ptr(lse_c)
+        check(lib.dkv_twocall_fwd(ctypes.byref(prm), _stream(q.device)), "two_call_split_fwd")
+    return out, lse_c, lse
+
+
+def two_call_split_bwd(q, k, v, p_rows: int, cu_seqlens, max_seqlen: int, softmax_scale: float,
+                       group_seq_cu, group_ctx_cu, out, lse_ctx, lse, d_out, deterministic: bool = False):
+    """-> (dQ, dK, dV) in the split layout; the prompt rows of dK / dV are the TOTAL prompt gradient
+    (Call 1 + Call 2 over every sequence of the group, fp32, cast once)."""
+    inp = _split_input(q, k, v, p_rows, cu_seqlens, max_seqlen, softmax_scale, group_seq_cu, group_ctx_cu)
+    q_ctx = _check_prompt_q(q[:p_rows], inp)
+    out, d_out = out.contiguous(), d_out.to(q.dtype).contiguous()
+    with torch.cuda.device(q.device):
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        # the gradients go straight into the split-layout buffers
+        prm2, _, keep = _bwd_params(inp.q, inp.k_context, inp.v_context, inp.k_decoded, inp.v_decoded, inp.cu_dev,
+                                    inp.num_sequences, p_rows, inp._grid_max, inp.softmax_scale, out[p_rows:], lse,
+                                    d_out[p_rows:], deterministic, groups=inp._groups,
+                                    grads=(dq[p_rows:], dk[:p_rows], dv[:p_rows], dk[p_rows:], dv[p_rows:]))
+        prm = TwoCallBwdParams()
+        prm.call2 = prm2
+        prm.q_ctx, prm.out_ctx, prm.lse_ctx = _ptr(q_ctx), _ptr(out[:p_rows]), _ptr(lse_ctx.contiguous())
+        prm.dout_ctx, prm.dq_ctx = _ptr(d_out[:p_rows]), _ptr(dq[:p_rows])
+        ws_bytes = int(lib.dkv_twocall_bwd_workspace_size(ctypes.byref(prm)))
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)
+        check(lib.dkv_twocall_bwd(ctypes.byref(prm), ws.data_ptr(), ws_bytes, _stream(q.device)),
+              "two_call_split_bwd")
+        del keep
+    return dq, dk, dv

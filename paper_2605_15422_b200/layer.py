@@ -74,7 +74,8 @@ class DualKVBatch:
 
 
 def _rms_norm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
-    """Per-head RMSNorm over head_dim (Qwen3 q_norm / k_norm), fp32 statistics."""
+    """Per-head RMSNorm over head_dim (Qwen3 q_norm / k_norm), fp32 statistics -- the unfused torch
+    composition the fused `dualkv::qkv_prep` kernel is tested against."""
     xf = x.float()
     return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps) * w.float()).to(x.dtype)
 
@@ -89,13 +90,27 @@ class DualKVSelfAttention(torch.nn.Module):
         self.scale = 1.0 / math.sqrt(head_dim)
         mk = lambda i, o: torch.nn.Parameter(
             (torch.randn(i, o, device=device) / math.sqrt(i)).to(dtype))
-        self.w_q, self.w_k, self.w_v = mk(d_model, heads * head_dim), mk(d_model, kv_heads * head_dim), \
-            mk(d_model, kv_heads * head_dim)
+        # one [d_model, (H + 2 H_k) d] projection: a single GEMM whose output rows feed the fused
+        # norm + RoPE + split epilogue
+        self.w_qkv = mk(d_model, (heads + 2 * kv_heads) * head_dim)
         self.w_o = mk(heads * head_dim, d_model)
         self.qk_norm = qk_norm
         if qk_norm:
             self.q_norm = torch.nn.Parameter(torch.ones(head_dim, device=device, dtype=dtype))
             self.k_norm = torch.nn.Parameter(torch.ones(head_dim, device=device, dtype=dtype))
+
+    # column views of the fused projection (W_Q, W_K, W_V of the reference block)
+    @property
+    def w_q(self):
+        return self.w_qkv[:, :self.h * self.d]
+
+    @property
+    def w_k(self):
+        return self.w_qkv[:, self.h * self.d:(self.h + self.hk) * self.d]
+
+    @property
+    def w_v(self):
+        return self.w_qkv[:, (self.h + self.hk) * self.d:]
 
     def forward(self, x: torch.Tensor, batch: Union[DualKVBatch, PackPlan]) -> torch.Tensor:
         """x: [T_dk, d_model] hidden states of the P+NR rows; returns the block's output projection
@@ -105,17 +120,13 @@ class DualKVSelfAttention(torch.nn.Module):
         if x.shape[0] != batch.total:
             raise ValueError(f"expected {batch.total} rows, got {x.shape[0]}")
         t = x.shape[0]
-        q = (x @ self.w_q).view(t, self.h, self.d)
-        k = (x @ self.w_k).view(t, self.hk, self.d)
-        v = (x @ self.w_v).view(t, self.hk, self.d)
-        if self.qk_norm:
-            q, k = _rms_norm(q, self.q_norm, self.eps), _rms_norm(k, self.k_norm, self.eps)
-        q = torch.ops.dualkv.rope(q.contiguous(), batch.positions, self.base, False)
-        k = torch.ops.dualkv.rope(k.contiguous(), batch.positions, self.base, False)
-        pick = lambda a, rows: a.index_select(0, rows)
-        o_c, _, o_d, _ = torch.ops.dualkv.two_call_fwd(
-            pick(q, batch.ctx_rows), pick(k, batch.ctx_rows), pick(v, batch.ctx_rows),
-            pick(q, batch.resp_rows), pick(k, batch.resp_rows), pick(v, batch.resp_rows),
-            batch.cu_seqlens, batch.max_seqlen, self.scale, batch.group_seq_cu, batch.group_ctx_cu)
-        o = torch.cat([o_c, o_d], dim=0).index_select(0, batch.inv_perm).reshape(t, self.h * self.d)
-        return o @ self.w_o
+        qkv = x @ self.w_qkv
+        # fused epilogue: q/k RMSNorm, RoPE at logical positions, scatter to [all prompts; all responses]
+        q, k, v = torch.ops.dualkv.qkv_prep(qkv, self.q_norm if self.qk_norm else None,
+                                            self.k_norm if self.qk_norm else None, batch.positions,
+                                            batch.inv_perm, self.h, self.hk, self.eps, self.base)
+        # every group's Call 1 + Call 2, one forward and one backward launch, on the split layout
+        o, _, _ = torch.ops.dualkv.two_call_split(q, k, v, batch.ctx_rows.shape[0], batch.cu_seqlens,
+                                                  batch.max_seqlen, self.scale, batch.group_seq_cu,
+                                                  batch.group_ctx_cu)
+        return o.index_select(0, batch.inv_perm).reshape(t, self.h * self.d) @ self.w_o

@@ -27,7 +27,7 @@ from torch import Tensor
 from . import api
 from .api import DualKVInput
 
-__all__ = ["attention", "two_call_attention", "rope"]
+__all__ = ["attention", "two_call_attention", "rope"]  # + dualkv::qkv_prep (the fused QKV epilogue)
 
 
 def _input(q, kc, vc, kd, vd, cu, max_seqlen, scale, gs, gc) -> DualKVInput:
@@ -204,3 +204,108 @@ torch.library.register_autograd("dualkv::rope", _rope_backward, setup_context=_r
 def rope(x: Tensor, positions: Tensor, base: float = 10000.0) -> Tensor:
     """[T, heads, d] rotated at device int64 `positions` [T] (autograd-enabled)."""
     return torch.ops.dualkv.rope(x, positions, float(base), False)
+
+
+# ---------------------------------------------------------------- fused QKV epilogue
+@torch.library.custom_op("dualkv::qkv_prep", mutates_args=(), device_types="cuda")
+def _qkv_prep(qkv: Tensor, q_norm: Optional[Tensor], k_norm: Optional[Tensor], positions: Tensor, dst_rows: Tensor,
+              heads: int, kv_heads: int, eps: float, base: float) -> Tuple[Tensor, Tensor, Tensor]:
+    from .rope import qkv_prep
+    return qkv_prep(qkv, q_norm, k_norm, positions, dst_rows, heads, kv_heads, eps, base)
+
+
+@_qkv_prep.register_fake
+def _qkv_prep_fake(qkv, q_norm, k_norm, positions, dst_rows, heads, kv_heads, eps, base):
+    t = qkv.shape[0]
+    d = qkv.numel() // (t * (heads + 2 * kv_heads)) if t else 0
+    return (qkv.new_empty((t, heads, d)), qkv.new_empty((t, kv_heads, d)), qkv.new_empty((t, kv_heads, d)))
+
+
+@torch.library.custom_op("dualkv::qkv_prep_bwd", mutates_args=(), device_types="cuda")
+def _qkv_prep_bwd(dq: Tensor, dk: Tensor, dv: Tensor, qkv: Tensor, q_norm: Optional[Tensor],
+                  k_norm: Optional[Tensor], positions: Tensor, dst_rows: Tensor, heads: int, kv_heads: int,
+                  eps: float, base: float) -> Tuple[Tensor, Tensor, Tensor]:
+    from .rope import qkv_prep_backward
+    dqkv, dwq, dwk = qkv_prep_backward(dq, dk, dv, qkv, q_norm, k_norm, positions, dst_rows, heads, kv_heads, eps,
+                                       base)
+    if dwq is None:  # custom ops return tensors: empty placeholders for "no norm"
+        dwq = dwk = qkv.new_empty((0,), dtype=torch.float32)
+    return dqkv, dwq, dwk
+
+
+@_qkv_prep_bwd.register_fake
+def _qkv_prep_bwd_fake(dq, dk, dv, qkv, q_norm, k_norm, positions, dst_rows, heads, kv_heads, eps, base):
+    n = dq.shape[-1] if q_norm is not None else 0
+    return torch.empty_like(qkv), qkv.new_empty((n,), dtype=torch.float32), qkv.new_empty((n,), dtype=torch.float32)
+
+
+def _qkv_setup(ctx, inputs, output):
+    qkv, q_norm, k_norm, positions, dst_rows, heads, kv_heads, eps, base = inputs
+    ctx.save_for_backward(qkv, q_norm, k_norm, positions, dst_rows)
+    ctx.meta = (heads, kv_heads, eps, base)
+
+
+def _qkv_backward(ctx, dq, dk, dv):
+    qkv, q_norm, k_norm, positions, dst_rows = ctx.saved_tensors
+    heads, kv_heads, eps, base = ctx.meta
+    zeros = lambda like, n: like.new_zeros((like.shape[0], n, like.shape[-1]))
+    dq = zeros(qkv, heads) if dq is None else dq
+    dk = zeros(qkv, kv_heads) if dk is None else dk
+    dv = zeros(qkv, kv_heads) if dv is None else dv
+    dqkv, dwq, dwk = torch.ops.dualkv.qkv_prep_bwd(dq, dk, dv, qkv, q_norm, k_norm, positions, dst_rows, heads,
+                                                  kv_heads, eps, base)
+    dqn = dwq.to(q_norm.dtype) if q_norm is not None else None
+    dkn = dwk.to(k_norm.dtype) if k_norm is not None else None
+    return dqkv, dqn, dkn, None, None, None, None, None, None
+
+
+torch.library.register_autograd("dualkv::qkv_prep", _qkv_backward, setup_context=_qkv_setup)
+
+
+# ---------------------------------------------------------------- two-call op on the split layout
+@torch.library.custom_op("dualkv::two_call_split", mutates_args=(), device_types="cuda")
+def _split_fwd(q: Tensor, k: Tensor, v: Tensor, p_rows: int, cu_seqlens: Tensor, max_seqlen: int,
+               softmax_scale: float, group_seq_cu: List[int], group_ctx_cu: List[int]) -> Tuple[Tensor, Tensor, Tensor]:
+    return api.two_call_split_fwd(q, k, v, p_rows, cu_seqlens, max_seqlen, softmax_scale, group_seq_cu,
+                                  group_ctx_cu)
+
+
+@_split_fwd.register_fake
+def _split_fwd_fake(q, k, v, p_rows, cu_seqlens, max_seqlen, softmax_scale, group_seq_cu, group_ctx_cu):
+    h = q.shape[1]
+    return (torch.empty_like(q), q.new_empty((h, p_rows), dtype=torch.float32),
+            q.new_empty((h, q.shape[0] - p_rows), dtype=torch.float32))
+
+
+@torch.library.custom_op("dualkv::two_call_split_bwd", mutates_args=(), device_types="cuda")
+def _split_bwd(q: Tensor, k: Tensor, v: Tensor, p_rows: int, cu_seqlens: Tensor, max_seqlen: int,
+               softmax_scale: float, group_seq_cu: List[int], group_ctx_cu: List[int], out: Tensor, lse_ctx: Tensor,
+               lse: Tensor, d_out: Tensor, deterministic: bool) -> Tuple[Tensor, Tensor, Tensor]:
+    return api.two_call_split_bwd(q, k, v, p_rows, cu_seqlens, max_seqlen, softmax_scale, group_seq_cu,
+                                  group_ctx_cu, out, lse_ctx, lse, d_out, deterministic)
+
+
+@_split_bwd.register_fake
+def _split_bwd_fake(q, k, v, p_rows, cu_seqlens, max_seqlen, softmax_scale, group_seq_cu, group_ctx_cu, out,
+                    lse_ctx, lse, d_out, deterministic):
+    return torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+
+
+def _split_setup(ctx, inputs, output):
+    q, k, v, p_rows, cu, max_seqlen, scale, gs, gc = inputs
+    out, lse_c, lse = output
+    ctx.save_for_backward(q, k, v, cu, out, lse_c, lse)
+    ctx.meta = (p_rows, max_seqlen, scale, gs, gc)
+    ctx.mark_non_differentiable(lse_c, lse)
+
+
+def _split_backward(ctx, d_out, d_lc, d_l):
+    q, k, v, cu, out, lse_c, lse = ctx.saved_tensors
+    p_rows, max_seqlen, scale, gs, gc = ctx.meta
+    d_out = torch.zeros_like(out) if d_out is None else d_out.contiguous()
+    dq, dk, dv = torch.ops.dualkv.two_call_split_bwd(q, k, v, p_rows, cu, max_seqlen, scale, gs, gc, out, lse_c,
+                                                     lse, d_out, _deterministic())
+    return dq, dk, dv, None, None, None, None, None, None
+
+
+torch.library.register_autograd("dualkv::two_call_split", _split_backward, setup_context=_split_setup)

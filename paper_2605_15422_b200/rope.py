@@ -114,3 +114,55 @@ def repack_rope_to_dualkv(q_std: torch.Tensor, k_std: torch.Tensor, v_std: torch
                                         k_std.shape[1], q_std.shape[2], pos.data_ptr(), idx.data_ptr(),
                                         float(base), 0, _stream(q_std.device)), "rope_qkv_rows")
     return q, k, v
+
+
+def qkv_prep(qkv: torch.Tensor, q_norm: Optional[torch.Tensor], k_norm: Optional[torch.Tensor],
+             positions: torch.Tensor, dst_rows: torch.Tensor, heads: int, kv_heads: int, eps: float = 1e-6,
+             base: float = 10000.0) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """Fused epilogue of the QKV projection (`dkv_qkv_prep_fwd`): per-head q/k RMSNorm (Qwen3;
+    skipped when the weights are None), RoPE at logical positions, and the scatter of every packed
+    row r to row dst_rows[r] of q [T, H, d], k / v [T, H_k, d] -- one HBM pass."""
+    if not qkv.is_cuda or qkv.dtype != torch.bfloat16:
+        raise ValueError("qkv_prep: bf16 CUDA tensor required")
+    t = qkv.shape[0]
+    ht = heads + 2 * kv_heads
+    if qkv.numel() % max(1, t * ht) or (t and qkv.numel() // (t * ht) % 8):
+        raise ValueError(f"qkv_prep: qkv {tuple(qkv.shape)} is not [T, (H + 2 H_k) d]")
+    d = qkv.numel() // (t * ht) if t else 0
+    qkv = qkv.contiguous()
+    for name, x in (("positions", positions), ("dst_rows", dst_rows)):
+        if x.device != qkv.device or x.dtype != torch.int64 or tuple(x.shape) != (t,):
+            raise ValueError(f"qkv_prep: {name} must be int64 [{t}] on {qkv.device}")
+    w = [x.contiguous() if x is not None else None for x in (q_norm, k_norm)]
+    if (w[0] is None) != (w[1] is None):
+        raise ValueError("qkv_prep: q_norm and k_norm go together")
+    with torch.cuda.device(qkv.device):
+        q = torch.empty((t, heads, d), dtype=qkv.dtype, device=qkv.device)
+        k = torch.empty((t, kv_heads, d), dtype=qkv.dtype, device=qkv.device)
+        v = torch.empty_like(k)
+        check(lib.dkv_qkv_prep_fwd(qkv.data_ptr(), _p(w[0]), _p(w[1]), float(eps), positions.data_ptr(),
+                                   dst_rows.data_ptr(), q.data_ptr(), k.data_ptr(), v.data_ptr(), t, heads, kv_heads,
+                                   d, float(base), _stream(qkv.device)), "qkv_prep")
+    return q, k, v
+
+
+def qkv_prep_backward(dq, dk, dv, qkv, q_norm, k_norm, positions, dst_rows, heads: int, kv_heads: int,
+                      eps: float = 1e-6, base: float = 10000.0):
+    """Adjoint of `qkv_prep` -> (dqkv [T, (H + 2 H_k) d] in qkv's shape, dq_norm, dk_norm fp32 or None)."""
+    t, h, d = dq.shape
+    dq, dk, dv, qkv = dq.contiguous(), dk.contiguous(), dv.contiguous(), qkv.contiguous()
+    with torch.cuda.device(qkv.device):
+        dqkv = torch.empty_like(qkv)
+        dwq = dwk = None
+        if q_norm is not None:
+            dwq = torch.empty(d, dtype=torch.float32, device=qkv.device)
+            dwk = torch.empty(d, dtype=torch.float32, device=qkv.device)
+        check(lib.dkv_qkv_prep_bwd(dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), qkv.data_ptr(), _p(q_norm),
+                                   _p(k_norm), float(eps), positions.data_ptr(), dst_rows.data_ptr(),
+                                   dqkv.data_ptr(), _p(dwq), _p(dwk), t, heads, kv_heads, d, float(base),
+                                   _stream(qkv.device)), "qkv_prep_backward")
+    return dqkv, dwq, dwk
+
+
+def _p(x):
+    return None if x is None else x.data_ptr()

@@ -60,4 +60,4 @@ if os.environ.get("AB_REP", "1") == "1":
     out["rep_fwd"] = timed(rf, 3)
     o, l_ = sv["o"]
     out["rep_bwd"] = timed(lambda: dkv.fa2_varlen_bwd(rb, o, l_, dor), 3)
-print(json.dumps({"lib": os.environ.get("DKV_LIB", "libdkv.so"), **{k: round(v, 3) for k, v in out.items()}}))
+print(json.dumps({"lib": os.environ.get("DKV_LIB", "libdkv.so"), "label": os.environ.get("AB_LABEL"), **{k: round(v, 3) for k, v in out.items()}}))

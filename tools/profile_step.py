@@ -34,6 +34,8 @@ for _ in range(steps):
         dkv.fa2_varlen_bwd(ctx, oc, lc, doc)
     else:
         oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc, dec)
-        dkv.dualkv_two_call_bwd(qc, dec, oc, lc, doc, od, ld, dod, deterministic=False)
+        # DET=1: the ordered fold (per-chunk partial stores) instead of the atomic merge -- the
+        # difference in L2 reduction sectors isolates the dK_c / dV_c merge from the dQ reduce
+        dkv.dualkv_two_call_bwd(qc, dec, oc, lc, doc, od, ld, dod, deterministic=os.environ.get("DET") == "1")
 torch.cuda.synchronize()
 print("done")
