@@ -229,7 +229,7 @@ def _qkv_prep_bwd(dq: Tensor, dk: Tensor, dv: Tensor, qkv: Tensor, q_norm: Optio
     dqkv, dwq, dwk = qkv_prep_backward(dq, dk, dv, qkv, q_norm, k_norm, positions, dst_rows, heads, kv_heads, eps,
                                        base)
     if dwq is None:  # custom ops return tensors: empty placeholders for "no norm"
-        dwq = dwk = qkv.new_empty((0,), dtype=torch.float32)
+        dwq, dwk = qkv.new_empty((0,), dtype=torch.float32), qkv.new_empty((0,), dtype=torch.float32)
     return dqkv, dwq, dwk
 
 

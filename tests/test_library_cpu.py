@@ -8,7 +8,8 @@ from torch._subclasses.fake_tensor import FakeTensorMode
 
 import paper_2605_15422_b200  # noqa: F401  (registers the ops)
 
-OPS = ["fwd", "bwd", "two_call_fwd", "two_call_bwd", "rope"]
+OPS = ["fwd", "bwd", "two_call_fwd", "two_call_bwd", "rope", "qkv_prep", "qkv_prep_bwd", "two_call_split",
+       "two_call_split_bwd"]
 
 
 def _m(*shape, dt=torch.bfloat16):
@@ -19,7 +20,7 @@ def test_ops_registered_with_autograd():
     for name in OPS:
         op = getattr(torch.ops.dualkv, name)
         assert op.default._schema.name == f"dualkv::{name}"
-    for name in ("fwd", "two_call_fwd", "rope"):
+    for name in ("fwd", "two_call_fwd", "rope", "qkv_prep", "two_call_split"):
         assert torch._C._dispatch_has_kernel_for_dispatch_key(f"dualkv::{name}", "Autograd")
 
 
