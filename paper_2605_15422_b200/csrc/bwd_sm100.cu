@@ -53,6 +53,9 @@ constexpr int kDrainT0 = kWDrain * 32;  // first drain thread
 #define BWD_POLY 0  // sweep 0/2/4/6: 27.5/27.7/28.1/27.9 ms (noise-level; MUFU is not the limit here)
 #endif
 constexpr int kPolyPairs = BWD_POLY;    // of every 16 exponential pairs, on the FMA pipe
+#ifndef BWD_SPIN
+#define BWD_SPIN 0
+#endif
 #ifndef BWD_OWN_ORDER
 // own-response items: 0 kv head fastest, then sequence, then key tile; 1 key tile fastest within
 // (sequence, kv head).  A/B at C3 (profiles/r2_ab.md): 1 is 1.5x faster on the causal N-copy
@@ -337,12 +340,22 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       auto koff_kv = [](int k) { return static_cast<uint64_t>(((k >> 2) * kKVPanel + (k & 3) * 32) >> 4); };
       auto koff_q = [](int k) { return static_cast<uint64_t>(((k >> 2) * kQPanel + (k & 3) * 32) >> 4); };
       auto koff_mn = [](int k) { return static_cast<uint64_t>((k * 2048) >> 4); };
-      mbar_wait(&bar.kv_full, 0);
+      // the issuer's waits are on the critical path of the tensor pipe: BWD_SPIN selects how it
+      // waits (0 try_wait with a suspend hint, 1 test_wait spin, 2 try_wait without a hint)
+      auto issuer_wait = [](uint64_t* b, uint32_t ph) {
+        if constexpr (BWD_SPIN == 1)
+          mbar_spin(b, ph);
+        else if constexpr (BWD_SPIN == 2)
+          mbar_wait_nohint(b, ph);
+        else
+          mbar_wait(b, ph);
+      };
+      issuer_wait(&bar.kv_full, 0);
       for (int i = 0; i <= nq; ++i) {
         if (i < nq) {
           const int st = i % kStages;
-          mbar_wait(&bar.q_full[st], (i / kStages) & 1);
-          if (i > 0) mbar_wait(&bar.sdp_empty, (i - 1) & 1);
+          issuer_wait(&bar.q_full[st], (i / kStages) & 1);
+          if (i > 0) issuer_wait(&bar.sdp_empty, (i - 1) & 1);
           tc_fence_after();
           const uint64_t dQk = sdesc_sw128(smem_u32(base + kOffQ + st * kQBytes), 16, 1024);
           const uint64_t dOk = sdesc_sw128(smem_u32(base + kOffDO + st * kQBytes), 16, 1024);
@@ -363,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
           const int sj = j % kStages;
           const uint64_t dQm = sdesc_sw128(smem_u32(base + kOffQ + sj * kQBytes), kQPanel, 1024);
           const uint64_t dOm = sdesc_sw128(smem_u32(base + kOffDO + sj * kQBytes), kQPanel, 1024);
-          mbar_wait(&bar.pds_full, j & 1);
+          issuer_wait(&bar.pds_full, j & 1);
           tc_fence_after();
           TRACE(T_ISS_DV, j);
 #pragma unroll
@@ -373,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
           for (int k = 0; k < kBQ / 16; ++k)
             mma_ts(tdK, tDS + k * 8, dQm + koff_mn(k), id_kv, (j > 0 || k > 0) ? 1u : 0u);
           mma_commit(&bar.q_empty[sj]);
-          mbar_wait(&bar.dq_empty, (j & 1) ^ 1);
+          issuer_wait(&bar.dq_empty, (j & 1) ^ 1);
           tc_fence_after();
           TRACE(T_ISS_DQ, j);
 #pragma unroll

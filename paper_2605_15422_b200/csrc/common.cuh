@@ -129,6 +129,37 @@ DKV_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Non-suspending waits for latency-critical single threads (the MMA issuers): a try_wait with a
+// suspend-time hint was traced waking ~500 clk after the phase completed (tools/trace_bwd.py).
+DKV_DEVICE bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+DKV_DEVICE void mbar_spin(uint64_t* bar, uint32_t parity) {
+  while (!mbar_test(bar, parity)) {
+  }
+}
+// try_wait without a suspend-time hint (the implementation's default window)
+DKV_DEVICE void mbar_wait_nohint(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
 // generic-proxy smem writes -> visible to the async proxy (UMMA / TMA reads)
 DKV_DEVICE void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 

@@ -46,6 +46,9 @@ constexpr int kPolyPairs = FWD_POLY;       // of every 16 exponential pairs, on 
 // L2 hint of the own-region K/V tiles: 0 evict_last (as the prompt's), 1 normal, 2 first
 #define FWD_EVICT 1
 #endif
+#ifndef FWD_SPIN
+#define FWD_SPIN 0
+#endif
 #ifndef FWD_ORDER
 // main work-item order: 0 kv head fastest, then sequence, then q block; 1 q block fastest within
 // (sequence, kv head).  A/B at C3 (tools/ab.sh, profiles/r2_ab.md): 1 + evict-normal own K/V is
@@ -352,9 +355,14 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
           mma_commit(bar);
       };
       // pair mode: these barriers complete from the peer CTA too -> poll (see mbar_wait_poll)
+      // (FWD_SPIN: 1 test_wait spin, 2 try_wait without a suspend hint -- see mbar_spin)
       auto wait = [&](uint64_t* bar, uint32_t ph) {
         if constexpr (kPair)
           mbar_wait_poll(bar, ph);
+        else if constexpr (FWD_SPIN == 1)
+          mbar_spin(bar, ph);
+        else if constexpr (FWD_SPIN == 2)
+          mbar_wait_nohint(bar, ph);
         else
           mbar_wait(bar, ph);
       };
