@@ -1,5 +1,6 @@
 """Small two-call DualKV fwd+bwd (ragged, partial tiles, R_i = 0, G = 4), a d = 64 DualKV fwd+bwd,
-and the fused repack+RoPE gather, for compute-sanitizer."""
+the fused repack+RoPE gather, a multi-group two-call launch (one group with an empty prompt), the
+fused QKV epilogue (norm + RoPE + scatter) and the attention layer fwd+bwd, for compute-sanitizer."""
 import os, sys
 import numpy as np
 import torch
@@ -24,6 +25,25 @@ from paper_2605_15422_b200 import packing as pk  # noqa: E402
 plan = pk.make_plan([(p, rl), (31, [5, 64])])
 xs = [mk(plan.total_standard, hh, d) for hh in (h, hk, hk)]
 rq, rk, rv = dkv.repack_rope_to_dualkv(*xs, plan, 1e6)
+# multi-group launch: three groups (one with P = 0) in one fwd and one bwd launch
+groups = [(130, [40, 0, 77]), (0, [19]), (257, [128, 3])]
+pc = sum(x[0] for x in groups)
+lens = [r for _, rs in groups for r in rs]
+tt = sum(lens)
+mq, mkc, mvc, mdoc = mk(pc, h, d), mk(pc, hk, d), mk(pc, hk, d), mk(pc, h, d)
+mqd, mkd, mvd, mdod = mk(tt, h, d), mk(tt, hk, d), mk(tt, hk, d), mk(tt, h, d)
+gs = np.concatenate([[0], np.cumsum([len(rs) for _, rs in groups])])
+gc = np.concatenate([[0], np.cumsum([x[0] for x in groups])])
+minp = dkv.DualKVInput(mqd, mkc, mvc, mkd, mvd, np.concatenate([[0], np.cumsum(lens)]), group_seq_cu=gs, group_ctx_cu=gc)
+moc, mlc, mod, mld = dkv.dualkv_two_call_fwd(mq, minp)
+mg = dkv.dualkv_two_call_bwd(mq, minp, moc, mlc, mdoc, mod, mld, mdod, deterministic=False, return_context_f32=True)
+# the attention layer: one QKV GEMM, fused q/k norm + RoPE + scatter, every group in one launch
+from paper_2605_15422_b200.layer import DualKVSelfAttention  # noqa: E402
+blk = DualKVSelfAttention(128, h, hk, d, rope_base=1e6, qk_norm=True)
+lplan = pk.make_plan(groups)
+x = mk(lplan.total_dualkv, 128).requires_grad_()
+y = blk(x, lplan)
+y.backward(torch.ones_like(y))
 torch.cuda.synchronize()
 print("ok", [float(x.float().abs().sum()) for x in gr], float(rq.float().abs().sum() + rk.float().abs().sum()),
       [float(x.float().abs().sum()) for x in g64])
