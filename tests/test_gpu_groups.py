@@ -117,3 +117,42 @@ def test_layer_compiles_fullgraph_and_matches_eager(cuda_device):
     for n in g0:
         err = (g1[n].float() - g0[n].float()).abs().max().item() / max(g0[n].float().abs().max().item(), 1e-30)
         assert err < 2e-2, f"compiled grad {n}: {err:.3e}"
+
+
+def test_c4_groups_one_launch_equals_per_group_launches(cuda_device):
+    """C4-sized groups (P = 8K, N = 16, R_i ~ U[512, 4096] with the bench's group seeds), four of
+    them in one launch each way vs one launch per group."""
+    import paper_2605_15422_b200 as dkv
+    p, h, hk, d = 8192, 32, 8, 128
+    rls = [[int(x) for x in np.random.default_rng(gi).integers(512, 4097, 16)] for gi in range(4)]
+    g = torch.Generator(device="cuda").manual_seed(5)
+    per = []
+    for rl in rls:
+        t = sum(rl)
+        per.append(dict(qc=_rand(g, p, h, d), kc=_rand(g, p, hk, d), vc=_rand(g, p, hk, d), doc=_rand(g, p, h, d),
+                        q=_rand(g, t, h, d), kd=_rand(g, t, hk, d), vd=_rand(g, t, hk, d), dod=_rand(g, t, h, d),
+                        cu=np.concatenate([[0], np.cumsum(rl)]).astype(np.int64)))
+    cat = lambda k: torch.cat([x[k] for x in per]).contiguous()
+    lens = [r for rl in rls for r in rl]
+    inp = dkv.DualKVInput(cat("q"), cat("kc"), cat("vc"), cat("kd"), cat("vd"), np.concatenate([[0], np.cumsum(lens)]),
+                          group_seq_cu=np.arange(0, 65, 16), group_ctx_cu=np.arange(0, 4 * p + 1, p))
+    qc_all, doc_all = cat("qc"), cat("doc")
+    oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc_all, inp)
+    dq_c, dkc, dvc, dq, dkd, dvd = dkv.dualkv_two_call_bwd(qc_all, inp, oc, lc, doc_all, od, ld, cat("dod"),
+                                                           deterministic=False)
+    r0 = 0
+    for gi, x in enumerate(per):
+        t = int(x["cu"][-1])
+        one = dkv.DualKVInput(x["q"], x["kc"], x["vc"], x["kd"], x["vd"], x["cu"])
+        f = dkv.dualkv_two_call_fwd(x["qc"], one)
+        b = dkv.dualkv_two_call_bwd(x["qc"], one, f[0], f[1], x["doc"], f[2], f[3], x["dod"], deterministic=False)
+        torch.cuda.synchronize()
+        c = slice(gi * p, (gi + 1) * p)
+        assert torch.equal(oc[c], f[0]) and torch.equal(od[r0:r0 + t], f[2]), f"group {gi} forward"
+        assert torch.equal(ld[:, r0:r0 + t], f[3]) and torch.equal(lc[:, c], f[1])
+        assert torch.equal(dkd[r0:r0 + t], b[4]) and torch.equal(dvd[r0:r0 + t], b[5]), f"group {gi} dK_d/dV_d"
+        for got, ref, name in ((dq[r0:r0 + t], b[3], "dQ"), (dq_c[c], b[0], "dQ_ctx"), (dkc[c], b[1], "dK_c"),
+                               (dvc[c], b[2], "dV_c")):
+            rel = ((got.float() - ref.float()).abs().max() / ref.float().abs().max()).item()
+            assert rel < 1e-2, f"group {gi} {name}: {rel:.2e}"
+        r0 += t
