@@ -276,6 +276,20 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       reinterpret_cast<uint4*>(base + kOffK + kKVPanel)[i] = make_uint4(0u, 0u, 0u, 0u);
     fence_async_smem();
   }
+  // G not dividing 64 (e.g. G = 5): a query tile is tq = 64 / G (floored) tokens x G heads; the
+  // TMA boxes fill its first qrows rows only, so the padding rows of every Q / dO stage are zeroed
+  // once (their S^T / dP^T columns are then finite and masked to P = dS = 0)
+  const int qrows = p.tq * p.group;
+  if (qrows < kBQ) {
+    for (int st = 0; st < kStages; ++st)
+      for (int pn = 0; pn < D / 64; ++pn)
+        for (int i = threadIdx.x; i < (kBQ - qrows) * 8; i += kThreads) {
+          const int off = (qrows + i / 8) * 128 + (i % 8) * 16;
+          *reinterpret_cast<uint4*>(base + kOffQ + st * kQBytes + pn * kQPanel + off) = make_uint4(0u, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(base + kOffDO + st * kQBytes + pn * kQPanel + off) = make_uint4(0u, 0u, 0u, 0u);
+        }
+    fence_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -308,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         mbar_wait(&bar.q_empty[st], ph ^ 1);
         TRACE(T_Q_LOAD, i);
         const int row0 = cu[it.s] + it.tok;
-        mbar_arrive_expect_tx(&bar.q_full[st], ((DKV_ABL(p.ablate) & 4) ? 0 : 2 * kQBytes) + 2 * kXBytes);
+        mbar_arrive_expect_tx(&bar.q_full[st], ((DKV_ABL(p.ablate) & 4) ? 0 : 2 * qrows * D * 2) + 2 * kXBytes);
         for (int pn = 0; pn < D / 64 && !(DKV_ABL(p.ablate) & 4); ++pn) {
           tma_load_3d(base + kOffQ + st * kQBytes + pn * kQPanel, mq, &bar.q_full[st], pn * 64, hk * G, row0);
           tma_load_3d(base + kOffDO + st * kQBytes + pn * kQPanel, mdo, &bar.q_full[st], pn * 64, hk * G, row0);
@@ -432,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
         const int dt = key - it.tok;
         cmin = dt <= 0 ? 0 : min(dt * G, kBQ);
       }
-      const int cmax = min(kBQ, (it.rlen - it.tok) * G);
+      const int cmax = min(qrows, (it.rlen - it.tok) * G);
       const float2 sl2 = make_float2(p.scale_log2, p.scale_log2);
       uint32_t pp[16], pd[16];
       // S' = S - lse/scale and dP' = dP - D arrive from the MMA: P = exp2(S' scale log2e),
@@ -514,6 +528,22 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       // r1_microbench.md), so the staging of one half overlaps the other half's egress
       if (DKV_ABL(p.ablate) & 1) continue;
       const int row0 = cu[it.s] + it.tok;
+      if (qrows < kBQ) {
+        // G not dividing 64: one reduce of the tile's tq x G rows (a 32-row half would split a token)
+        float* stg = reinterpret_cast<float*>(base + kOffStage);
+        if (threadIdx.x == kDrainT0) bulk_wait_read<0>();  // the previous tile's reduce has read it
+        named_bar_sync(1, 128);
+#pragma unroll
+        for (int c = 0; c < kBQ; ++c)
+          if (c < qrows && (D == 128 || d < D)) stg[c * D + d] = __uint_as_float(u[c]);
+        fence_async_smem();
+        named_bar_sync(1, 128);
+        if (threadIdx.x == kDrainT0) {
+          tma_reduce_add_3d(mdq, stg, 0, hk * G, row0);
+          bulk_commit();
+        }
+        continue;
+      }
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         float* stg = reinterpret_cast<float*>(base + kOffStage + hh * (kStageBytes / 2));
@@ -595,7 +625,7 @@ DKV_TRACE_READ_FN(dkv_trace_read_v1)
 static bool tc_bwd1_supported(int head_dim, int heads, int kv_heads) {
   if ((head_dim != 64 && head_dim != 128) || kv_heads <= 0 || heads % kv_heads) return false;
   const int G = heads / kv_heads;
-  return G <= bwd::kBQ && (bwd::kBQ % G) == 0;
+  return G <= bwd::kBQ;  // a 64-row query tile holds floor(64 / G) tokens x G heads
 }
 
 bool tc_bwd_supported(int dtype, int head_dim, int heads, int kv_heads) {
@@ -610,7 +640,9 @@ static int launch(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp,
   Params p{};
   const int G = a.heads / a.kv_heads;
   const int tq = kBQ / G;
-  const int hb = G < kBQ / 2 ? G : kBQ / 2, tb = (kBQ / 2) / hb;  // dQ reduce box: one 32-row half
+  // dQ reduce box: one 32-row half when G divides 64, else the tile's whole tq x G rows
+  const bool halves = kBQ % G == 0;
+  const int hb = !halves ? G : (G < kBQ / 2 ? G : kBQ / 2), tb = !halves ? tq : (kBQ / 2) / hb;
   if (a.total_q > 0 &&
       (!make_map_3d_bf16(&p.tm_q, a.q, a.total_q, a.heads, D, G, tq) ||
        !make_map_3d_bf16(&p.tm_do, a.dout, a.total_q, a.heads, D, G, tq) ||

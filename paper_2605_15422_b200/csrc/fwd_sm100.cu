@@ -254,7 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
           for (int pn = 0; pn < C::kPanels; ++pn)
             tma_load_3d_2sm(sQ[t] + pn * C::kPanelBytes, mq, lq, pn * 64, hk * p.group, seq0 + tok0 + t * p.tq);
       } else {
-        const int qbytes = C::kPanelBytes * C::kPanels * (has_b ? 2 : 1);
+        // a tile is tq x G rows of 128 B per 64-column panel (< 128 rows when G does not divide 128)
+        const int qbytes = p.tq * p.group * 128 * C::kPanels * (has_b ? 2 : 1);
         mbar_arrive_expect_tx(&sm.q_full, qbytes);
         for (int t = 0; t < (has_b ? 2 : 1); ++t)
           for (int pn = 0; pn < C::kPanels; ++pn)
@@ -418,7 +419,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     const bool tile_ok = (t == 0) || has_b;
     const int qtok = tok0 + t * p.tq + row / p.group;  // sequence-local token of this row
     const int head = hk * p.group + row % p.group;
-    const bool row_valid = tile_ok && qtok < rlen;
+    // G not dividing 128 (e.g. Qwen3-14B, G = 5): a tile holds tq = 128 / G (floored) tokens x G
+    // heads; its last 128 - tq G rows are padding (stale smem rows, computed, never stored)
+    const bool row_valid = tile_ok && qtok < rlen && row < p.tq * p.group;
     const int qmin = tok0 + t * p.tq;                  // first token of the tile
     const int cb = 64 * h;                             // first key column of this half
     constexpr int kDH = D / 2;                         // O columns this half rescales / stores
@@ -597,7 +600,7 @@ int launch(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, cudaSt
       return DKV_ERR_CUDA;
     }
   }
-  const bool pair = D == 128 && fwd_pairs();
+  const bool pair = D == 128 && fwd_pairs() && tq * G == kBM;  // pair mode: full tiles only
   if (pair && ((a.total_q > 0 && !make_map_3d_bf16(&p.tm_k64, a.k, a.total_q, a.kv_heads, D, 1, 64)) ||
                (a.ctx_len > 0 && !make_map_3d_bf16(&p.tm_kc64, a.k_ctx, a.ctx_len, a.kv_heads, D, 1, 64)))) {
     set_error("cuTensorMapEncodeTiled failed for the pair-mode K maps");
@@ -686,7 +689,7 @@ bool tc_supported(int dtype, int head_dim, int heads, int kv_heads) {
   if (head_dim != 64 && head_dim != 128) return false;
   if (kv_heads <= 0 || heads % kv_heads) return false;
   const int G = heads / kv_heads;
-  return G <= 128 && (128 % G) == 0;
+  return G <= 128;  // a 128-row query tile holds floor(128 / G) tokens x G heads
 }
 
 int launch_tc_fwd(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, cudaStream_t st) {

@@ -52,7 +52,9 @@ def test_tensor_core_dispatch_table():
     assert f(_lib.DKV_BF16, 64, 8, 8) == 1
     assert f(_lib.DKV_F32, 64, 8, 8) == 0         # C1 fp32 -> SIMT fp32 kernels
     assert f(_lib.DKV_BF16, 8, 4, 2) == 0         # reference sweep head dims -> SIMT
-    assert f(_lib.DKV_BF16, 128, 12, 4) == 0      # G = 3 does not divide 128
+    assert f(_lib.DKV_BF16, 128, 12, 4) == 1      # G = 3: tiles of 42 tokens x 3 heads (2 padding rows)
+    assert f(_lib.DKV_BF16, 128, 40, 8) == 1      # Qwen3-14B / Qwen2.5-14B, G = 5
+    assert f(_lib.DKV_BF16, 128, 130, 1) == 0     # G > 128 -> SIMT
 
 
 def test_costmodel_matches_oracle():
