@@ -64,6 +64,10 @@ CONFIGS = {
                     "+ overlapped fp32 gradient all-reduce"),
     "C5": dict(n=32, p=16384, r=2048, h=32, hk=4, d=128, dtype="bf16", groups=8, scaling="weak",
                desc="C5: Qwen3-30B-A3B attention (32/4 heads) N=32 P=16K R=2K, 8 groups per GPU in one launch"),
+    # not a BASELINE config: the C3 workload at Qwen3-14B heads (40 / 8, G = 5 does not divide the
+    # tile rows -> padded query tiles)
+    "Q14": dict(n=32, p=8192, r=2048, h=40, hk=8, d=128, dtype="bf16", groups=1, scaling="weak",
+                desc="Qwen3-14B attention (40/8 heads, G=5) N=32 P=8K R=2K (extra, not a BASELINE config)"),
 }
 # the CPU sample: full heads, a full C2-size prompt, one full response (bounded: ~7e11 FLOP/step)
 CPU_SAMPLE = dict(n=1, p=4096, r=1024, h=32, hk=8, d=128)
