@@ -228,7 +228,9 @@ static int auto_chunk(const dkv_bwd_params* p, const GroupTable& g) {
   if (p->ctx_len == 0) return static_cast<int>(nmax);
   const bool tc = tc_bwd_supported(p->dtype, static_cast<int>(p->head_dim), static_cast<int>(p->heads),
                                    static_cast<int>(p->kv_heads));
-  if (!tc) return static_cast<int>(nmax);  // SIMT: one ordered fold over all sequences
+  // SIMT: a warp per (prompt key, kv head, chunk) walks the chunk's query rows serially; up to 16
+  // chunks (one sequence each for N <= 16) keep those warps short, folded in fixed order
+  if (!tc) return static_cast<int>((nmax + 15) / 16);
   // enough context units to fill ~8 waves of the SMs, but no more than needed
   const int64_t n_ctx_tiles = (g.max_ctx + 127) / 128;
   const int64_t units_per_chunk = std::max<int64_t>(1, n_ctx_tiles * p->kv_heads * g.n);

@@ -8,6 +8,8 @@
 // and cast once.
 #include "dkv_internal.h"
 
+#include <type_traits>
+
 namespace dkv {
 
 template <typename T>
@@ -30,7 +32,18 @@ DKV_DEVICE float warp_sum(float v) {
   return v;
 }
 
-constexpr int kMaxPerLane = 8;  // head_dim <= 256
+// values per lane of a head_dim row: a template parameter of every kernel (2 / 4 / 8 for head_dim
+// <= 64 / 128 / 256), so small head dims do not pay registers for 256
+constexpr int kKeyBlock = 4;    // keys (fwd, dQ) / query rows (dK dV) per step: independent dot
+                                // products and interleaved shuffle reductions (ILP over the chain)
+
+template <int N>
+DKV_DEVICE void warp_sum_n(float (&v)[N]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+}
 
 // cu_seqlens entry i; a null cu means one sequence spanning all total_q rows (the prompt of a
 // fused two-call launch)
@@ -49,7 +62,7 @@ DKV_DEVICE int seq_of_row(const int32_t* cu, int n, int t) {
 
 // ---------------------------------------------------------------- forward
 // one warp per (packed query row, head); lanes split head_dim
-template <typename T>
+template <typename T, int kMaxPerLane>
 __global__ void simt_fwd_kernel(SimtArgs a) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -69,31 +82,51 @@ __global__ void simt_fwd_kernel(SimtArgs a) {
     acc[i] = 0.f;
   }
   float m = -INFINITY, l = 0.f;
-  auto visit = [&](const T* kbase, const T* vbase, int j) {
-    const T* kr = kbase + (static_cast<int64_t>(j) * a.kv_heads + hk) * D;
-    float part = 0.f;
+  // keys j0 .. j0 + cnt - 1 (cnt <= kKeyBlock) in one online-softmax step
+  auto visit = [&](const T* kbase, const T* vbase, int j0, int cnt) {
+    float sc[kKeyBlock];
 #pragma unroll
-    for (int i = 0; i < kMaxPerLane; ++i) {
-      int e = lane + 32 * i;
-      if (e < D) part += qr[i] * ldf(kr + e);
+    for (int b = 0; b < kKeyBlock; ++b) {
+      sc[b] = 0.f;
+      if (b < cnt) {
+        const T* kr = kbase + (static_cast<int64_t>(j0 + b) * a.kv_heads + hk) * D;
+#pragma unroll
+        for (int i = 0; i < kMaxPerLane; ++i) {
+          int e = lane + 32 * i;
+          if (e < D) sc[b] += qr[i] * ldf(kr + e);
+        }
+      }
     }
-    float sc = warp_sum(part) * a.scale;
-    float mn = fmaxf(m, sc);
-    float alpha = expf(m - mn);  // m = -inf first time -> 0
-    float p = expf(sc - mn);
-    l = l * alpha + p;
-    const T* vr = vbase + (static_cast<int64_t>(j) * a.kv_heads + hk) * D;
+    warp_sum_n(sc);
+    float mn = m;
+#pragma unroll
+    for (int b = 0; b < kKeyBlock; ++b) {
+      sc[b] = b < cnt ? sc[b] * a.scale : -INFINITY;
+      mn = fmaxf(mn, sc[b]);
+    }
+    const float alpha = expf(m - mn);  // m = -inf first time -> 0
+    float pb[kKeyBlock];
+#pragma unroll
+    for (int b = 0; b < kKeyBlock; ++b) pb[b] = b < cnt ? expf(sc[b] - mn) : 0.f;
+    l = l * alpha + ((pb[0] + pb[1]) + (pb[2] + pb[3]));
 #pragma unroll
     for (int i = 0; i < kMaxPerLane; ++i) {
       int e = lane + 32 * i;
-      if (e < D) acc[i] = acc[i] * alpha + p * ldf(vr + e);
+      if (e < D) {
+        float add = 0.f;
+#pragma unroll
+        for (int b = 0; b < kKeyBlock; ++b)
+          if (b < cnt) add += pb[b] * ldf(vbase + (static_cast<int64_t>(j0 + b) * a.kv_heads + hk) * D + e);
+        acc[i] = acc[i] * alpha + add;
+      }
     }
     m = mn;
   };
-  for (int j = 0; j < a.ctx_len; ++j) visit(static_cast<const T*>(a.k_ctx), static_cast<const T*>(a.v_ctx), j);
+  for (int j = 0; j < a.ctx_len; j += kKeyBlock)
+    visit(static_cast<const T*>(a.k_ctx), static_cast<const T*>(a.v_ctx), j, min(kKeyBlock, a.ctx_len - j));
   const T* kown = static_cast<const T*>(a.k) + static_cast<int64_t>(seq0) * a.kv_heads * D;
   const T* vown = static_cast<const T*>(a.v) + static_cast<int64_t>(seq0) * a.kv_heads * D;
-  for (int j = 0; j <= r; ++j) visit(kown, vown, j);
+  for (int j = 0; j <= r; j += kKeyBlock) visit(kown, vown, j, min(kKeyBlock, r + 1 - j));
   T* o = static_cast<T*>(a.out) + (static_cast<int64_t>(t) * a.heads + h) * D;
   const float inv = 1.f / l;
 #pragma unroll
@@ -106,7 +139,7 @@ __global__ void simt_fwd_kernel(SimtArgs a) {
 
 // ---------------------------------------------------------------- backward: dQ
 // D_row[h, t] = sum_d dO*O computed by the preprocess kernel (fa2.py:232-234)
-template <typename T>
+template <typename T, int kMaxPerLane>
 __global__ void simt_bwd_dq_kernel(SimtArgs a, const float* drow) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -128,31 +161,44 @@ __global__ void simt_bwd_dq_kernel(SimtArgs a, const float* drow) {
   }
   const float lse = a.lse[static_cast<int64_t>(h) * a.total_q + t];
   const float dr = drow[static_cast<int64_t>(h) * a.total_q + t];
-  auto visit = [&](const T* kbase, const T* vbase, int j) {
-    const int64_t ko = (static_cast<int64_t>(j) * a.kv_heads + hk) * D;
-    float sp = 0.f, dp = 0.f;
+  auto visit = [&](const T* kbase, const T* vbase, int j0, int cnt) {
+    float sp[kKeyBlock], dp[kKeyBlock];
 #pragma unroll
-    for (int i = 0; i < kMaxPerLane; ++i) {
-      int e = lane + 32 * i;
-      if (e < D) {
-        sp += qr[i] * ldf(kbase + ko + e);
-        dp += gr[i] * ldf(vbase + ko + e);
+    for (int b = 0; b < kKeyBlock; ++b) {
+      sp[b] = 0.f;
+      dp[b] = 0.f;
+      if (b < cnt) {
+        const int64_t ko = (static_cast<int64_t>(j0 + b) * a.kv_heads + hk) * D;
+#pragma unroll
+        for (int i = 0; i < kMaxPerLane; ++i) {
+          int e = lane + 32 * i;
+          if (e < D) {
+            sp[b] += qr[i] * ldf(kbase + ko + e);
+            dp[b] += gr[i] * ldf(vbase + ko + e);
+          }
+        }
       }
     }
-    sp = warp_sum(sp);
-    dp = warp_sum(dp);
-    float p = expf(sp * a.scale - lse);
-    float ds = p * (dp - dr) * a.scale;
+    warp_sum_n(sp);
+    warp_sum_n(dp);
 #pragma unroll
-    for (int i = 0; i < kMaxPerLane; ++i) {
-      int e = lane + 32 * i;
-      if (e < D) dq[i] += ds * ldf(kbase + ko + e);
+    for (int b = 0; b < kKeyBlock; ++b) {
+      if (b >= cnt) break;
+      const float p = expf(sp[b] * a.scale - lse);
+      const float ds = p * (dp[b] - dr) * a.scale;
+      const int64_t ko = (static_cast<int64_t>(j0 + b) * a.kv_heads + hk) * D;
+#pragma unroll
+      for (int i = 0; i < kMaxPerLane; ++i) {
+        int e = lane + 32 * i;
+        if (e < D) dq[i] += ds * ldf(kbase + ko + e);
+      }
     }
   };
-  for (int j = 0; j < a.ctx_len; ++j) visit(static_cast<const T*>(a.k_ctx), static_cast<const T*>(a.v_ctx), j);
+  for (int j = 0; j < a.ctx_len; j += kKeyBlock)
+    visit(static_cast<const T*>(a.k_ctx), static_cast<const T*>(a.v_ctx), j, min(kKeyBlock, a.ctx_len - j));
   const T* kown = static_cast<const T*>(a.k) + static_cast<int64_t>(seq0) * a.kv_heads * D;
   const T* vown = static_cast<const T*>(a.v) + static_cast<int64_t>(seq0) * a.kv_heads * D;
-  for (int j = 0; j <= r; ++j) visit(kown, vown, j);
+  for (int j = 0; j <= r; j += kKeyBlock) visit(kown, vown, j, min(kKeyBlock, r + 1 - j));
 #pragma unroll
   for (int i = 0; i < kMaxPerLane; ++i) {
     int e = lane + 32 * i;
@@ -166,7 +212,7 @@ __global__ void simt_bwd_dq_kernel(SimtArgs a, const float* drow) {
 // sums over every query row of sequences [s_begin, s_end) (a "chunk"), in
 // sequence order, into fp32, then either casts once (ctx_out_*) or writes the
 // fp32 partial (instrumentation / deterministic fold).
-template <typename T>
+template <typename T, int kMaxPerLane>
 __global__ void simt_bwd_dkv_kernel(SimtArgs a, const float* drow, int own_rows, int chunk,
                                     int num_chunks, float* ctx_part, float* own_part) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -213,28 +259,39 @@ __global__ void simt_bwd_dkv_kernel(SimtArgs a, const float* drow, int own_rows,
   for (int s = s_lo; s < s_hi; ++s) {
     const int r0 = cu_at(a, s), r1 = cu_at(a, s + 1);
     const int first = is_ctx ? r0 : r0 + j;
-    for (int t = first; t < r1; ++t) {
-      for (int g = 0; g < G; ++g) {
-        const int h = hk * G + g;
+    // (query row, head) pairs of the sequence, kKeyBlock at a time (row-major, head fastest)
+    const int n_pairs = (r1 - first) * G;
+    for (int q0 = 0; q0 < n_pairs; q0 += kKeyBlock) {
+      float sp[kKeyBlock], dp[kKeyBlock];
+      float qv[kKeyBlock][kMaxPerLane], gv[kKeyBlock][kMaxPerLane];
+#pragma unroll
+      for (int b = 0; b < kKeyBlock; ++b) {
+        sp[b] = 0.f;
+        dp[b] = 0.f;
+        const bool live = q0 + b < n_pairs;
+        const int t = first + (q0 + b) / G, h = hk * G + (q0 + b) % G;
         const int64_t qo = (static_cast<int64_t>(t) * a.heads + h) * D;
-        float sp = 0.f, dp = 0.f;
-        float qv[kMaxPerLane], gv[kMaxPerLane];
 #pragma unroll
         for (int i = 0; i < kMaxPerLane; ++i) {
           int e = lane + 32 * i;
-          qv[i] = e < D ? ldf(static_cast<const T*>(a.q) + qo + e) : 0.f;
-          gv[i] = e < D ? ldf(static_cast<const T*>(a.dout) + qo + e) : 0.f;
-          sp += qv[i] * kr[i];
-          dp += gv[i] * vr[i];
+          qv[b][i] = (live && e < D) ? ldf(static_cast<const T*>(a.q) + qo + e) : 0.f;
+          gv[b][i] = (live && e < D) ? ldf(static_cast<const T*>(a.dout) + qo + e) : 0.f;
+          sp[b] += qv[b][i] * kr[i];
+          dp[b] += gv[b][i] * vr[i];
         }
-        sp = warp_sum(sp);
-        dp = warp_sum(dp);
-        const float p = expf(sp * a.scale - a.lse[static_cast<int64_t>(h) * a.total_q + t]);
-        const float ds = p * (dp - drow[static_cast<int64_t>(h) * a.total_q + t]) * a.scale;
+      }
+      warp_sum_n(sp);
+      warp_sum_n(dp);
+#pragma unroll
+      for (int b = 0; b < kKeyBlock; ++b) {
+        if (q0 + b >= n_pairs) break;
+        const int t = first + (q0 + b) / G, h = hk * G + (q0 + b) % G;
+        const float p = expf(sp[b] * a.scale - a.lse[static_cast<int64_t>(h) * a.total_q + t]);
+        const float ds = p * (dp[b] - drow[static_cast<int64_t>(h) * a.total_q + t]) * a.scale;
 #pragma unroll
         for (int i = 0; i < kMaxPerLane; ++i) {
-          dv[i] += p * gv[i];
-          dk[i] += ds * qv[i];
+          dv[i] += p * gv[b][i];
+          dk[i] += ds * qv[b][i];
         }
       }
     }
@@ -275,38 +332,54 @@ __global__ void simt_bwd_dkv_kernel(SimtArgs a, const float* drow, int own_rows,
   }
 }
 
+// head_dim -> values per lane
+template <typename F>
+static void by_lanes(int head_dim, F&& f) {
+  if (head_dim <= 64)
+    f(std::integral_constant<int, 2>{});
+  else if (head_dim <= 128)
+    f(std::integral_constant<int, 4>{});
+  else
+    f(std::integral_constant<int, 8>{});
+}
+
 void launch_simt_fwd(const SimtArgs& a, cudaStream_t st) {
   const int64_t warps = a.total_q * a.heads;
   if (warps == 0) return;
   const int threads = 256;
   const int64_t blocks = (warps * 32 + threads - 1) / threads;
-  if (a.dtype == DKV_F32)
-    simt_fwd_kernel<float><<<blocks, threads, 0, st>>>(a);
-  else
-    simt_fwd_kernel<__nv_bfloat16><<<blocks, threads, 0, st>>>(a);
+  by_lanes(a.head_dim, [&](auto pl) {
+    if (a.dtype == DKV_F32)
+      simt_fwd_kernel<float, decltype(pl)::value><<<blocks, threads, 0, st>>>(a);
+    else
+      simt_fwd_kernel<__nv_bfloat16, decltype(pl)::value><<<blocks, threads, 0, st>>>(a);
+  });
 }
 
 void launch_simt_bwd(const SimtArgs& a, const float* drow, int chunk, int num_chunks, float* ctx_part,
                      float* own_part, cudaStream_t st) {
   const int threads = 256;
   const int64_t w1 = a.total_q * a.heads;
-  if (w1 > 0) {
-    const int64_t b1 = (w1 * 32 + threads - 1) / threads;
-    if (a.dtype == DKV_F32)
-      simt_bwd_dq_kernel<float><<<b1, threads, 0, st>>>(a, drow);
-    else
-      simt_bwd_dq_kernel<__nv_bfloat16><<<b1, threads, 0, st>>>(a, drow);
-  }
   const int64_t w2 = a.total_q * a.kv_heads + a.ctx_len * a.kv_heads * num_chunks;
-  if (w2 > 0) {
-    const int64_t b2 = (w2 * 32 + threads - 1) / threads;
-    if (a.dtype == DKV_F32)
-      simt_bwd_dkv_kernel<float><<<b2, threads, 0, st>>>(a, drow, static_cast<int>(a.total_q), chunk,
-                                                         num_chunks, ctx_part, own_part);
-    else
-      simt_bwd_dkv_kernel<__nv_bfloat16><<<b2, threads, 0, st>>>(a, drow, static_cast<int>(a.total_q),
-                                                                 chunk, num_chunks, ctx_part, own_part);
-  }
+  by_lanes(a.head_dim, [&](auto pl) {
+    constexpr int PL = decltype(pl)::value;
+    if (w1 > 0) {
+      const int64_t b1 = (w1 * 32 + threads - 1) / threads;
+      if (a.dtype == DKV_F32)
+        simt_bwd_dq_kernel<float, PL><<<b1, threads, 0, st>>>(a, drow);
+      else
+        simt_bwd_dq_kernel<__nv_bfloat16, PL><<<b1, threads, 0, st>>>(a, drow);
+    }
+    if (w2 > 0) {
+      const int64_t b2 = (w2 * 32 + threads - 1) / threads;
+      if (a.dtype == DKV_F32)
+        simt_bwd_dkv_kernel<float, PL><<<b2, threads, 0, st>>>(a, drow, static_cast<int>(a.total_q), chunk,
+                                                               num_chunks, ctx_part, own_part);
+      else
+        simt_bwd_dkv_kernel<__nv_bfloat16, PL><<<b2, threads, 0, st>>>(a, drow, static_cast<int>(a.total_q),
+                                                                       chunk, num_chunks, ctx_part, own_part);
+    }
+  });
 }
 
 }  // namespace dkv
