@@ -646,7 +646,8 @@ def two_call_split_bwd(q, k, v, p_rows: int, cu_seqlens, max_seqlen: int, softma
                                     grads=(dq[p_rows:], dk[:p_rows], dv[:p_rows], dk[p_rows:], dv[p_rows:]))
         prm = TwoCallBwdParams()
         prm.call2 = prm2
-        prm.q_ctx, prm.out_ctx, prm.lse_ctx = _ptr(q_ctx), _ptr(out[:p_rows]), _ptr(lse_ctx.contiguous())
+        lse_ctx = lse_ctx.to(torch.float32).contiguous()  # kept alive until the launch is enqueued
+        prm.q_ctx, prm.out_ctx, prm.lse_ctx = _ptr(q_ctx), _ptr(out[:p_rows]), _ptr(lse_ctx)
         prm.dout_ctx, prm.dq_ctx = _ptr(d_out[:p_rows]), _ptr(dq[:p_rows])
         ws_bytes = int(lib.dkv_twocall_bwd_workspace_size(ctypes.byref(prm)))
         ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)
