@@ -738,6 +738,15 @@ def run_layer(args, cfg, dkv, torch, dist, world, rank, dev, my_r, fl_job, timed
     proj_fl_rank = 3 * 2 * rows * dm * (h + 2 * hk) * d + 3 * 2 * rows * h * d * dm  # QKV + O proj, fwd+bwd
     fl_attn_rank = 14 * sum(visible_pairs(p, rl, "dualkv") for rl in my_r) * h * d
     attn_ms = (fms + bms) / max(1, args.steps)
+    # the device repack alone (report it against HBM bandwidth): the input rows of
+    # every micro-batch gathered from the replicated layout, read + written once
+    rp_ms = timed(lambda: [pk.repack_to_dualkv(x_std[:pl.total_standard], pl) for pl, _ in mbs], args.steps)
+    rp_bytes = 2 * rows * dm * 2
+    hbm = _peaks().get("hbm_gbs")
+    repack = {"ms_per_step": round(rp_ms, 3), "bytes": rp_bytes,
+              "GB_per_s": round(rp_bytes / (rp_ms * 1e-3) / 1e9, 1),
+              "frac_of_hbm": round(rp_bytes / (rp_ms * 1e-3) / 1e9 / hbm, 3) if hbm else None,
+              "what": "repack_to_dualkv of every micro-batch's hidden states (d_model wide rows), N(P+R) -> P+NR"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world,
@@ -757,6 +766,7 @@ def run_layer(args, cfg, dkv, torch, dist, world, rank, dev, my_r, fl_job, timed
             "attention_kernels_ms_per_step_rank0": round(attn_ms, 3),
             "attention_kernel_tflops_rank0": round(fl_attn_rank / (attn_ms * 1e-3) / 1e12, 2) if attn_ms else None,
             "attention_share_of_step": round(attn_ms / ms, 3),
+            "repack": repack,
             "roofline": {"bound": "tensor", "kernel": "dualkv_bwd_kernel (multi-group launch)",
                          "achieved": round(10 * fl_attn_rank / 14 * args.steps / (bms * 1e-3) / 1e12, 2)
                          if bms else None, "peak": peak_sus, "unit": "TFLOP/s",

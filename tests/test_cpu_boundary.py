@@ -65,3 +65,21 @@ def test_costmodel_matches_oracle():
             assert costmodel.visible_pairs(p, rl, mode) == orc.visible_pairs(p, rl, mode)
     # headline numbers quoted in BASELINE.md (C3)
     assert costmodel.attention_flops(8192, [2048] * 32, 32, 128, passes="fwdbwd") == 36560875552768  # 3.656e13
+
+
+def test_integration_stub_matches_the_abi():
+    """The reference-side ctypes stub printed in INTEGRATION.md §2 lays out dkv_fwd_params exactly
+    like the library's own binding (field names, order, sizes)."""
+    import ctypes as C
+    from paper_2605_15422_b200 import _lib
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    block = text.split("```python", 1)[1].split("```", 1)[0]
+    src = "\n".join(ln for ln in block.splitlines()
+                    if not ln.startswith(("_lib", "assert _lib", "import torch")) and "CDLL" not in ln)
+    ns = {}
+    exec(compile("import ctypes\n" + src.split("def dualkv_fwd_gpu")[0], "INTEGRATION.md", "exec"), ns)
+    stub, ours = ns["_Fwd"], _lib.FwdParams
+    assert C.sizeof(stub) == C.sizeof(ours)
+    assert [f[0] for f in stub._fields_] == [f[0] for f in ours._fields_]
+    for name, _ in ours._fields_:
+        assert getattr(stub, name).offset == getattr(ours, name).offset, name
