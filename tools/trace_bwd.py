@@ -27,8 +27,7 @@ oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc, dec)
 run = lambda: dkv.dualkv_two_call_bwd(qc, dec, oc, lc, doc, od, ld, dod, deterministic=False)
 run()
 torch.cuda.synchronize()
-V2 = os.environ.get("DKV_BWD_V2") == "1"
-fn = lib.dkv_trace_read if V2 else lib.dkv_trace_read_v1
+fn = lib.dkv_trace_read_v1
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
 buf = np.zeros((16, 256), dtype=np.int64)
 fn(None, cta)
@@ -48,14 +47,9 @@ valid = [i for i in range(1, 256) if rel[2, i] > 0 and rel[2, i - 1] > 0]
 if valid:
     per = np.diff(rel[2, [0] + valid])
     print("median tile period", float(np.median(per)), "clk over", len(valid), "tiles")
-    if V2:
-        pairs_ = [("S issue -> compute sees S", 2, 7), ("compute S -> P done", 7, 8), ("dP issue -> compute sees dP", 3, 9),
-                  ("compute dP -> dS done", 9, 10), ("dQ issue -> drain sees dQ", 6, 11), ("drain dQ -> loaded", 11, 12),
-                  ("drain loaded -> chunks issued", 12, 13), ("dQ issue -> next dP issue", 6, 3)]
-    else:
-        pairs_ = [("Q/dO load issue -> arrival", 0, 1), ("S issue -> compute sees S+dP", 2, 7), ("compute TMEM loads", 7, 9), ("compute math", 9, 8), ("compute waits pds_empty+stores", 8, 10),
-                  ("pds_full -> dV issue", 10, 4), ("dV issue -> dQ issue", 4, 6), ("dQ issue -> drain sees dQ", 6, 11),
-                  ("drain dQ -> loaded", 11, 12), ("drain loaded -> halves issued", 12, 13)]
+    pairs_ = [("Q/dO load issue -> arrival", 0, 1), ("S issue -> compute sees S+dP", 2, 7), ("compute TMEM loads", 7, 9), ("compute math", 9, 8), ("compute waits pds_empty+stores", 8, 10),
+              ("pds_full -> dV issue", 10, 4), ("dV issue -> dQ issue", 4, 6), ("dQ issue -> drain sees dQ", 6, 11),
+              ("drain dQ -> loaded", 11, 12), ("drain loaded -> halves issued", 12, 13)]
     for nm, a, b in pairs_:
         if b == 3:
             dd = [rel[3, i + 1] - rel[6, i] for i in valid[:-1] if rel[3, i + 1] > 0]
