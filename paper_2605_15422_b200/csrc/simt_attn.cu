@@ -34,8 +34,10 @@ DKV_DEVICE float warp_sum(float v) {
 
 // values per lane of a head_dim row: a template parameter of every kernel (2 / 4 / 8 for head_dim
 // <= 64 / 128 / 256), so small head dims do not pay registers for 256
-constexpr int kKeyBlock = 4;    // keys (fwd, dQ) / query rows (dK dV) per step: independent dot
-                                // products and interleaved shuffle reductions (ILP over the chain)
+// keys (fwd, dQ) / query rows (dK dV) per step: independent dot products and interleaved shuffle
+// reductions (ILP over the L2-latency-bound chain); more for small head dims (fewer registers per row)
+template <int kMaxPerLane>
+constexpr int key_block() { return kMaxPerLane <= 2 ? 8 : (kMaxPerLane <= 4 ? 4 : 2); }
 
 template <int N>
 DKV_DEVICE void warp_sum_n(float (&v)[N]) {
@@ -64,6 +66,7 @@ DKV_DEVICE int seq_of_row(const int32_t* cu, int n, int t) {
 // one warp per (packed query row, head); lanes split head_dim
 template <typename T, int kMaxPerLane>
 __global__ void simt_fwd_kernel(SimtArgs a) {
+  constexpr int kKeyBlock = kMaxPerLane <= 4 ? 4 : 2;  // (8 measured slower here: register-bound)
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= a.total_q * a.heads) return;
@@ -108,7 +111,10 @@ __global__ void simt_fwd_kernel(SimtArgs a) {
     float pb[kKeyBlock];
 #pragma unroll
     for (int b = 0; b < kKeyBlock; ++b) pb[b] = b < cnt ? expf(sc[b] - mn) : 0.f;
-    l = l * alpha + ((pb[0] + pb[1]) + (pb[2] + pb[3]));
+    float psum = 0.f;
+#pragma unroll
+    for (int b = 0; b < kKeyBlock; ++b) psum += pb[b];
+    l = l * alpha + psum;
 #pragma unroll
     for (int i = 0; i < kMaxPerLane; ++i) {
       int e = lane + 32 * i;
@@ -141,6 +147,7 @@ __global__ void simt_fwd_kernel(SimtArgs a) {
 // D_row[h, t] = sum_d dO*O computed by the preprocess kernel (fa2.py:232-234)
 template <typename T, int kMaxPerLane>
 __global__ void simt_bwd_dq_kernel(SimtArgs a, const float* drow) {
+  constexpr int kKeyBlock = key_block<kMaxPerLane>();
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= a.total_q * a.heads) return;
@@ -215,6 +222,7 @@ __global__ void simt_bwd_dq_kernel(SimtArgs a, const float* drow) {
 template <typename T, int kMaxPerLane>
 __global__ void simt_bwd_dkv_kernel(SimtArgs a, const float* drow, int own_rows, int chunk,
                                     int num_chunks, float* ctx_part, float* own_part) {
+  constexpr int kKeyBlock = kMaxPerLane <= 4 ? 4 : 2;  // (8 measured slower here)
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int D = a.head_dim;
