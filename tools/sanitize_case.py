@@ -44,6 +44,11 @@ lplan = pk.make_plan(groups)
 x = mk(lplan.total_dualkv, 128).requires_grad_()
 y = blk(x, lplan)
 y.backward(torch.ones_like(y))
+# GQA ratio that does not divide the tile rows (G = 5, Qwen3-14B): padded tiles, zeroed padding rows
+q5, kc5, vc5, kd5, vd5, do5 = mk(t, 20, d), mk(p, 4, d), mk(p, 4, d), mk(t, 4, d), mk(t, 4, d), mk(t, 20, d)
+in5 = dkv.DualKVInput(q5, kc5, vc5, kd5, vd5, np.concatenate([[0], np.cumsum(rl)]))
+o5, l5 = dkv.dualkv_fwd(in5)
+g5 = dkv.dualkv_bwd(in5, o5, l5, do5, deterministic=False)
 torch.cuda.synchronize()
 print("ok", [float(x.float().abs().sum()) for x in gr], float(rq.float().abs().sum() + rk.float().abs().sum()),
       [float(x.float().abs().sum()) for x in g64])
