@@ -724,6 +724,7 @@ static int launch(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp,
 
 int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, const BwdScratch& w,
                   cudaStream_t st) {
+  if (tc_bwd_pair_supported(a.head_dim, a.heads, a.kv_heads)) return launch_tc_bwd_pair(a, self, grp, w, st);
   return a.head_dim == 64 ? bwd::launch<64>(a, self, grp, w, st) : bwd::launch<128>(a, self, grp, w, st);
 }
 

@@ -113,5 +113,9 @@ struct BwdScratch {
 };
 int launch_tc_bwd(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, const BwdScratch& w,
                   cudaStream_t st);
+// bwd_pair_sm100.cu: the CTA-pair backward (head_dim 128, G | 32), opt-in (DKV_BWD_PAIR=1)
+bool tc_bwd_pair_supported(int head_dim, int heads, int kv_heads);
+int launch_tc_bwd_pair(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, const BwdScratch& w,
+                       cudaStream_t st);
 
 }  // namespace dkv

@@ -44,7 +44,7 @@ def _run(tmp_path, name, env_extra):
     return torch.load(path)
 
 
-@pytest.mark.parametrize("switch", ["DKV_FWD_PAIR"])
+@pytest.mark.parametrize("switch", ["DKV_FWD_PAIR", "DKV_BWD_PAIR"])
 def test_variant_matches_default(switch, tmp_path, cuda_device):
     base = _run(tmp_path, "default", {})
     var = _run(tmp_path, switch, {switch: "1"})

@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2605_15422_b200 as dkv  # noqa: E402
 from paper_2605_15422_b200._lib import lib  # noqa: E402
 
-EV = ["Qld", "Qarr", "iS", "idP", "idV", "idK", "idQ", "cS", "cP", "cdP", "cdS", "dDQ", "dLD", "dEND", "mEND"]
+EV = ["Qld", "Qarr", "iS", "idP", "idV", "idK", "idQ", "cS", "cP", "cdP", "cdS", "dDQ", "dLD", "dEND", "mEND", "x15", "st", "kld"]
 cta = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 show = int(sys.argv[2]) if len(sys.argv) > 2 else 12
 n, p, r, h, hk, d = 32, 8192, 2048, 32, 8, 128
@@ -27,14 +27,14 @@ oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc, dec)
 run = lambda: dkv.dualkv_two_call_bwd(qc, dec, oc, lc, doc, od, ld, dod, deterministic=False)
 run()
 torch.cuda.synchronize()
-fn = lib.dkv_trace_read_v1
+fn = getattr(lib, os.environ.get("TRACE_FN", "dkv_trace_read_v1"))
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = np.zeros((16, 256), dtype=np.int64)
+buf = np.zeros((18, 256), dtype=np.int64)
 fn(None, cta)
 run()
 torch.cuda.synchronize()
 fn(buf.ctypes.data, -1)
-t0 = buf[buf > 0].min()
+t0 = buf[16, 0] if buf[16, 0] > 0 else buf[buf > 0].min()  # T_START when traced
 rel = np.where(buf > 0, buf - t0, -1)
 print("cta", cta, " columns: clk since the CTA's first event")
 print("tile " + " ".join(f"{e:>7}" for e in EV) + "  period(iS)")
@@ -42,12 +42,12 @@ for i in range(min(show, 256)):
     if rel[2, i] < 0 and rel[7, i] < 0:
         break
     per = rel[2, i] - rel[2, i - 1] if i > 0 and rel[2, i - 1] >= 0 else 0
-    print(f"{i:4d} " + " ".join(f"{rel[e, i]:7d}" for e in range(15)) + f"  {per}")
+    print(f"{i:4d} " + " ".join(f"{rel[e, i]:7d}" for e in list(range(16)) + [17]) + f"  {per}")
 valid = [i for i in range(1, 256) if rel[2, i] > 0 and rel[2, i - 1] > 0]
 if valid:
     per = np.diff(rel[2, [0] + valid])
     print("median tile period", float(np.median(per)), "clk over", len(valid), "tiles")
-    pairs_ = [("Q/dO load issue -> arrival", 0, 1), ("S issue -> compute sees S+dP", 2, 7), ("compute TMEM loads", 7, 9), ("compute math", 9, 8), ("compute waits pds_empty+stores", 8, 10),
+    pairs_ = [("Q/dO load issue -> arrival", 0, 1), ("S issue -> compute sees S+dP", 2, 7), ("compute TMEM loads", 7, 9), ("compute math", 9, 8), ("compute waits pds_empty", 8, 14), ("compute stores+arrive", 14, 10),
               ("pds_full -> dV issue", 10, 4), ("dV issue -> dQ issue", 4, 6), ("dQ issue -> drain sees dQ", 6, 11),
               ("drain dQ -> loaded", 11, 12), ("drain loaded -> halves issued", 12, 13)]
     for nm, a, b in pairs_:
