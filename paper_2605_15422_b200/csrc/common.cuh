@@ -286,6 +286,13 @@ DKV_DEVICE uint32_t mapa_shared(const void* p, uint32_t rank) {
 DKV_DEVICE void mbar_arrive_remote(uint32_t rbar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
 }
+// Remote arrive without release semantics, for arrivals that publish no memory writes (e.g. "my
+// tcgen05.st / tcgen05.ld are complete", ordered by tcgen05.wait + fence::before_thread_sync):
+// a release at cluster scope compiles to MEMBAR.ALL.GPU (~1000+ clk under load), this to a bare
+// SYNCS.ARRIVE.RED.
+DKV_DEVICE void mbar_arrive_remote_relaxed(uint32_t rbar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
+}
 DKV_DEVICE void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t ok = 0;
   while (!ok) {

@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
             if (crank == 0)
               mbar_arrive(&sm.p_full[t]);
             else
-              mbar_arrive_remote(mapa_shared(&sm.p_full[t], 0));
+              mbar_arrive_remote_relaxed(mapa_shared(&sm.p_full[t], 0));  // P in TMEM: nothing to publish
           }
         } else {
           mbar_arrive(&sm.p_full[t]);
@@ -570,11 +570,14 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
   }
 }
 
-// DKV_FWD_PAIR=1: the CTA-pair (cta_group::2) forward for d = 128
+// The CTA-pair (cta_group::2) forward for d = 128 full tiles is the default since the peer's
+// P-ready arrive became relaxed (a release at cluster scope was a MEMBAR.ALL.GPU on the chain):
+// C3 forward 8.2-8.6 vs 8.5-8.7 ms single-CTA, interleaved (profiles/r2_ab.md).  DKV_FWD_PAIR=0
+// selects the single-CTA kernel.
 static bool fwd_pairs() {
   static const bool v = [] {
     const char* e = getenv("DKV_FWD_PAIR");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return v;
 }

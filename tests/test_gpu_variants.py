@@ -44,10 +44,12 @@ def _run(tmp_path, name, env_extra):
     return torch.load(path)
 
 
+# each switch flips one CTA-pair (cta_group::2) kernel against its single-CTA counterpart:
+# the forward pair is the default (DKV_FWD_PAIR=0 turns it off), the backward pair is opt-in
 @pytest.mark.parametrize("switch", ["DKV_FWD_PAIR", "DKV_BWD_PAIR"])
 def test_variant_matches_default(switch, tmp_path, cuda_device):
-    base = _run(tmp_path, "default", {})
-    var = _run(tmp_path, switch, {switch: "1"})
+    base = _run(tmp_path, "single", {"DKV_FWD_PAIR": "0", "DKV_BWD_PAIR": "0"})
+    var = _run(tmp_path, switch, {"DKV_FWD_PAIR": "0", "DKV_BWD_PAIR": "0", switch: "1"})
     for k, ref in base.items():
         got = var[k]
         tol = 1e-3 if k.startswith("l") else 2e-2
