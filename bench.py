@@ -632,7 +632,7 @@ def main():
     # ---- roofline of the dominant kernel (the backward main kernel)
     traffic, traffic_src = _traffic()
     tb = traffic.get("dualkv_bwd_kernel", {})
-    tf = traffic.get("dualkv_fwd_kernel<128>", {})
+    tf = traffic.get("dualkv_fwd_kernel", {})
     # per step each main kernel launches once (all groups, Call 1 fused into Call 2's launch):
     # achieved = algorithmic FLOPs of those launches / their device time (CUDA events by libdkv)
     bwd_ach = 10 * pairs_rank * h * d * args.steps / (bms * 1e-3) / 1e12 if bms else 0.0
@@ -647,7 +647,8 @@ def main():
             "traffic_source": f"{traffic_src} (ncu --set full, dram__bytes_read+write, one C3 launch)",
             "algorithmic_per_launch": "10 * visible_pairs * H * d FLOP (SURVEY 8d); "
                                       f"{10 * pairs_rank * h * d:.4e} per launch ({n_grp} group(s))",
-            "fwd_kernel": {"achieved": round(fwd_ach, 2), "frac": round(fwd_ach / peak_sus, 4),
+            "fwd_kernel": {"kernel": "dualkv_fwd_kernel<128, pair> (tcgen05 cta_group::2 CTA pair; Call 1 fused)",
+                           "achieved": round(fwd_ach, 2), "frac": round(fwd_ach / peak_sus, 4),
                            "frac_of_burst": round(fwd_ach / peak_burst, 4),
                            "traffic": (tf["dram_read_bytes"] + tf["dram_write_bytes"]) if tf else None},
             "kernel_ms": {"fwd_main_per_launch": round(fms / max(1, fl), 4),

@@ -19,7 +19,8 @@ sys.path.insert(0, sys.argv[1])
 import paper_2605_15422_b200 as dkv
 g = torch.Generator(device="cuda").manual_seed(3)
 mk = lambda *s: torch.randn(*s, device="cuda", generator=g).to(torch.bfloat16)
-p, rl, h, hk, d = 300, [77, 0, 520, 33, 129], 16, 4, 128
+p, rl, d = 300, [77, 0, 520, 33, 129], 128
+h, hk = int(sys.argv[3]), int(sys.argv[4])
 t = sum(rl)
 qc, kc, vc, doc = mk(p, h, d), mk(p, hk, d), mk(p, hk, d), mk(p, h, d)
 q, kd, vd, dod = mk(t, h, d), mk(t, hk, d), mk(t, hk, d), mk(t, h, d)
@@ -34,11 +35,11 @@ print(json.dumps({"ok": True}))
 """
 
 
-def _run(tmp_path, name, env_extra):
-    path = tmp_path / f"{name}.pt"
+def _run(tmp_path, name, env_extra, h, hk):
+    path = tmp_path / f"{name}_{h}_{hk}.pt"
     env = {**os.environ, **env_extra}
-    r = subprocess.run([sys.executable, "-c", _SCRIPT, ROOT, str(path)], env=env, capture_output=True, text=True,
-                       timeout=300)
+    r = subprocess.run([sys.executable, "-c", _SCRIPT, ROOT, str(path), str(h), str(hk)], env=env,
+                       capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     import torch
     return torch.load(path)
@@ -46,10 +47,11 @@ def _run(tmp_path, name, env_extra):
 
 # each switch flips one CTA-pair (cta_group::2) kernel against its single-CTA counterpart:
 # the forward pair is the default (DKV_FWD_PAIR=0 turns it off), the backward pair is opt-in
-@pytest.mark.parametrize("switch", ["DKV_FWD_PAIR", "DKV_BWD_PAIR"])
-def test_variant_matches_default(switch, tmp_path, cuda_device):
-    base = _run(tmp_path, "single", {"DKV_FWD_PAIR": "0", "DKV_BWD_PAIR": "0"})
-    var = _run(tmp_path, switch, {"DKV_FWD_PAIR": "0", "DKV_BWD_PAIR": "0", switch: "1"})
+@pytest.mark.parametrize("switch,h,hk", [("DKV_FWD_PAIR", 16, 4), ("DKV_FWD_PAIR", 32, 4), ("DKV_BWD_PAIR", 16, 4),
+                                         ("DKV_BWD_PAIR", 8, 8), ("DKV_BWD_PAIR", 32, 4), ("DKV_BWD_PAIR", 32, 2)])
+def test_variant_matches_default(switch, h, hk, tmp_path, cuda_device):
+    base = _run(tmp_path, "single", {"DKV_FWD_PAIR": "0", "DKV_BWD_PAIR": "0"}, h, hk)
+    var = _run(tmp_path, switch, {"DKV_FWD_PAIR": "0", "DKV_BWD_PAIR": "0", switch: "1"}, h, hk)
     for k, ref in base.items():
         got = var[k]
         tol = 1e-3 if k.startswith("l") else 2e-2
