@@ -16,6 +16,10 @@ dec = dkv.DualKVInput(q, kc, vc, kd, vd, np.concatenate([[0], np.cumsum(rl)]))
 oc, lc, od, ld = dkv.dualkv_two_call_fwd(qc, dec)
 for det in (True, False):
     gr = dkv.dualkv_two_call_bwd(qc, dec, oc, lc, doc, od, ld, dod, deterministic=det)
+if os.environ.get("SAN_SMALL"):  # racecheck on the cluster kernels is slow: the first case only
+    torch.cuda.synchronize()
+    print("ok small")
+    raise SystemExit(0)
 # d = 64 (tensor-core backward with the zero-padded K^T panel)
 q64, kc64, vc64, kd64, vd64, do64 = mk(t, h, 64), mk(p, hk, 64), mk(p, hk, 64), mk(t, hk, 64), mk(t, hk, 64), mk(t, h, 64)
 in64 = dkv.DualKVInput(q64, kc64, vc64, kd64, vd64, np.concatenate([[0], np.cumsum(rl)]))
