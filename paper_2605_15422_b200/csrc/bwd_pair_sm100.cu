@@ -365,12 +365,6 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
               " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sx + kXBytes)),
               "l"(reinterpret_cast<uint64_t>(mxh)), "r"(lq), "r"(16), "r"(xrow)
               : "memory");
-#if defined(DKV_TRACE) && defined(PAIR_TRACE_NLOAD)
-          if (rank == 0) {  // trace-only: the n part's arrival (delays this producer's next issue)
-            pwait(&bar.qn_full[st], ph);
-            TRACE(T_DO_LOAD, i);
-          }
-#endif
         }
         if (i > 0) {
           const int j = i - 1;
@@ -607,9 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
       named_bar_sync(1 + h, 64);
       if (issuer) {
         const int rr = h * 32;  // first tile row of the half: token rr / G, head rr % G
-#ifndef PAIR_NO_DQ_REDUCE  // (timing experiment: the dQ reduce-add's effect on the TMA load latency)
         tma_reduce_add_3d(mdq, stg, static_cast<int>(rank) * 64, hk * G + rr % G, row0 + rr / G);
-#endif
         bulk_commit();
       }
       if (threadIdx.x == kWDrain * 32) TRACE(T_D_END, i);
