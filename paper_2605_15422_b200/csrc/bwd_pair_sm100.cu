@@ -159,10 +159,12 @@ DKV_DEVICE void warp_arrive_leader_relaxed(uint64_t* bar, uint32_t rank) {
   }
 }
 
-// Every wait in the pair kernel polls (test_wait) with a short nanosleep between polls: a thread
-// suspended in try_wait was traced waking ~700-1100 clk after an arrival from the other CTA (remote
-// arrive, multicast commit, 2-SM TMA), while tight polling by several warps per sub-partition
-// starved the compute warps of issue slots.  PAIR_NS: the backoff in ns (-1: try_wait suspend).
+// Waits of the pair kernel.  A thread suspended in try_wait was traced waking several hundred clk
+// after an arrival from the other CTA (remote arrive, multicast commit, 2-SM TMA), but polling
+// (test_wait.acquire.cluster, with or without a nanosleep backoff) by several warps per
+// sub-partition starved the compute warps of issue slots and measured slower overall (C3: spin
+// 28.4, 32 ns backoff 27.5, 128 ns 27.9, suspend 27.0 ms).  PAIR_NS: -1 suspend (default), else the
+// polling backoff in ns.
 #ifndef PAIR_POLY
 #define PAIR_POLY 0  // of every 16 exponential pairs, computed on the FMA pipe
 #endif
