@@ -58,3 +58,14 @@ def test_variant_matches_default(switch, h, hk, tmp_path, cuda_device):
         err = ((got - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item() if not k.startswith("l") \
             else (got - ref).abs().max().item()
         assert err <= tol, f"{switch}: {k} differs from the default path by {err:.3e}"
+
+
+def test_pair_backward_at_headline_c3(cuda_device):
+    """The opt-in CTA-pair backward through the bench's exact call at full C3 against the
+    independent f64 slices (test_gpu_headline.py, run in a subprocess with the switch set)."""
+    env = {**os.environ, "DKV_BWD_PAIR": "1"}
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
+                        os.path.join(ROOT, "tests", "test_gpu_headline.py"), "-k", "C3 or c3"],
+                       env=env, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]
