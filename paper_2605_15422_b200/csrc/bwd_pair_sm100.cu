@@ -171,8 +171,15 @@ DKV_DEVICE void warp_arrive_leader_relaxed(uint64_t* bar, uint32_t rank) {
 #ifndef PAIR_NS
 #define PAIR_NS -1
 #endif
+#ifndef PAIR_NS_C
+#define PAIR_NS_C PAIR_NS  // compute warps' waits (S ready, P^T / dS^T buffers free)
+#endif
+#ifndef PAIR_NS_I
+#define PAIR_NS_I PAIR_NS  // MMA issuers' and the peer forwarder's waits
+#endif
+template <int NS = PAIR_NS>
 DKV_DEVICE void pwait(uint64_t* bar, uint32_t parity) {
-  if constexpr (PAIR_NS < 0) {
+  if constexpr (NS < 0) {
     mbar_wait(bar, parity);
   } else {
     for (;;) {
@@ -185,7 +192,7 @@ DKV_DEVICE void pwait(uint64_t* bar, uint32_t parity) {
           : "r"(smem_u32(bar)), "r"(parity)
           : "memory");
       if (ok) break;
-      if constexpr (PAIR_NS > 0) __nanosleep(PAIR_NS > 0 ? PAIR_NS : 0);
+      if constexpr (NS > 0) __nanosleep(NS > 0 ? NS : 0);
     }
   }
 }
@@ -398,11 +405,11 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
       const uint64_t dKk = sdesc_sw128(smem_u32(base + kOffK), 16, 1024);
       const uint64_t dVk = sdesc_sw128(smem_u32(base + kOffV), 16, 1024);
       const uint64_t dOnes = sdesc_sw32(smem_u32(base + kOffOnes));
-      pwait(&bar.kv_full, 0);
+      pwait<PAIR_NS_I>(&bar.kv_full, 0);
       for (int i = 0; i < nq; ++i) {
         const int st = i % kNSt;
-        pwait(&bar.qn_full[st], (i / kNSt) & 1);
-        if (i > 0) pwait(&bar.sdp_empty, (i - 1) & 1);
+        pwait<PAIR_NS_I>(&bar.qn_full[st], (i / kNSt) & 1);
+        if (i > 0) pwait<PAIR_NS_I>(&bar.sdp_empty, (i - 1) & 1);
         tc_fence_after();
         TRACE(T_ISS_S, i);
         const uint32_t sq = smem_u32(base + kOffQN + st * 2 * kQN);
@@ -417,13 +424,14 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
         mma_ss2(tdP, dOnes, dX + (kXBytes >> 4), id_sdp, 1u);
         mma_commit2_mc(&bar.sdp_full);
         mma_commit2_mc(&bar.qn_empty[st]);
+        TRACE(T_SISS_END, i);
       }
     } else if (rank == 0 && warp == kWMma2 && elect_one()) {
       const uint32_t id_kv = idesc_bf16_f32(2 * kBK, D, false, true);
       const uint32_t id_dq = idesc_bf16_f32(128, kBQ, true, true);
       const uint64_t dKT = sdesc_sw128(smem_u32(base + kOffKT), 0, 1024);
       const uint32_t sDS0 = smem_u32(base + kOffDS);
-      pwait(&bar.kv_full, 0);
+      pwait<PAIR_NS_I>(&bar.kv_full, 0);
       for (int j = 0; j < nq; ++j) {
         const int sj = j % kKSt;
         const uint32_t sq = smem_u32(base + kOffQK + sj * 2 * kQK);
@@ -431,9 +439,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
         const uint64_t dOm = sdesc_sw128(sq + kQK, 0, 1024);
         const int b = j & 1;
         mbar_arrive_expect_tx(&bar.ds_in[b], kDSBytes / 2);
-        pwait(&bar.pds_full, j & 1);
+        pwait<PAIR_NS_I>(&bar.pds_full, j & 1);
         TRACE(T_ISS_DP, j);
-        pwait(&bar.qk_full[sj], (j / kKSt) & 1);
+        pwait<PAIR_NS_I>(&bar.qk_full[sj], (j / kKSt) & 1);
         tc_fence_after();
         TRACE(T_ISS_DV, j);
 #pragma unroll
@@ -446,9 +454,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
         mma_commit2_mc(&bar.p_empty);
         // dQ^T of tile j: both CTAs' dS^T halves (ds_in: the peer's st.async bytes here + the peer
         // forwarder's report of the leader's bytes there) and a free dQ^T TMEM buffer
-        pwait(&bar.ds_in[b], (j >> 1) & 1);
+        pwait<PAIR_NS_I>(&bar.ds_in[b], (j >> 1) & 1);
         TRACE(T_ISS_DK, j);
-        pwait(&bar.dq_empty[b], ((j >> 1) & 1) ^ 1);
+        pwait<PAIR_NS_I>(&bar.dq_empty[b], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         fence_async_smem();  // the peer's st.async dS^T half -> visible to the tensor core
         TRACE(T_ISS_DQ, j);
@@ -460,6 +468,15 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
         mma_commit2_mc(&bar.ds_empty[b]);
       }
       mma_commit2_mc(&bar.kv_done);
+#ifdef DKV_TRACE
+    } else if (rank == 1 && warp == kWMma && elect_one()) {
+      // trace-only observer: when sdp_full actually completes in the peer (spinning, no suspend)
+      for (int i = 0; i < nq; ++i) {
+        while (!mbar_test(&bar.sdp_full, i & 1)) {
+        }
+        TRACE(T_SDONE, i);
+      }
+#endif
     } else if (rank == 1 && warp == kWMma2 && elect_one()) {
       // the peer's forwarder: once the leader's dS^T half of tile i has landed here (ds_in: st.async
       // bytes), make it visible to the tensor core and report to the leader's MMA issuer
@@ -467,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
         const int b = i & 1;
         const uint32_t lds = mapa_shared(&bar.ds_in[b], 0);
         mbar_arrive_expect_tx(&bar.ds_in[b], kDSBytes / 2);
-        pwait(&bar.ds_in[b], (i >> 1) & 1);
+        pwait<PAIR_NS_I>(&bar.ds_in[b], (i >> 1) & 1);
         TRACE(T_DO_LOAD, i);
         tc_fence_after();
         fence_async_smem();
@@ -491,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
     QIter it;
     it.begin(cu, p.tq, s0, s1, tok_first);
     for (int i = 0; it.valid(); it.next(), ++i) {
-      pwait(&bar.sdp_full, i & 1);
+      pwait<PAIR_NS_C>(&bar.sdp_full, i & 1);
       tc_fence_after();
       if (threadIdx.x == 0) TRACE(T_C_S, i);
       uint32_t us[32], ud[32];
@@ -539,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
       else
         math(std::true_type{});
       if (threadIdx.x == 0) TRACE(T_C_P, i);
-      pwait(&bar.p_empty, (i & 1) ^ 1);  // dV / dK of tile i - 1 done with P^T / dS^T
+      pwait<PAIR_NS_C>(&bar.p_empty, (i & 1) ^ 1);  // dV / dK of tile i - 1 done with P^T / dS^T
       tc_fence_after();
       if (threadIdx.x == 0) TRACE(T_MMA_END, i);
       tmem_st16(tmem + lane_off + 128 + c0 / 2, pp);
@@ -551,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
       // query half, once dQ^T of tile i - 2 is done with it; only dQ^T waits for these (ds_in), so
       // the stores and their proxy fence stay off the pds_full -> dV / dK -> p_empty loop
       const int b = i & 1;
-      pwait(&bar.ds_empty[b], ((i >> 1) & 1) ^ 1);
+      pwait<PAIR_NS_C>(&bar.ds_empty[b], ((i >> 1) & 1) ^ 1);
       if (ds_here) {
         uint8_t* ds_local = ds_local0 + b * kDSBytes;
 #pragma unroll

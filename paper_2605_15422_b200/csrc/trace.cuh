@@ -5,13 +5,13 @@
 
 namespace dkv {
 enum TraceEv { T_Q_LOAD, T_DO_LOAD, T_ISS_S, T_ISS_DP, T_ISS_DV, T_ISS_DK, T_ISS_DQ, T_C_S, T_C_P, T_C_DP, T_C_DS,
-               T_D_DQ, T_D_LD, T_D_END, T_MMA_END, T_EXTRA, T_START, T_KLOAD };
+               T_D_DQ, T_D_LD, T_D_END, T_MMA_END, T_EXTRA, T_START, T_KLOAD, T_SISS_END, T_SDONE };
 }
 
 #ifdef DKV_TRACE
 namespace dkv {
 constexpr int kTraceTiles = 256;
-constexpr int kTraceEvents = 18;
+constexpr int kTraceEvents = 20;
 static __device__ long long g_trace[kTraceEvents * kTraceTiles];
 static __device__ int g_trace_cta = -1;
 }  // namespace dkv

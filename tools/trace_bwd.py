@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2605_15422_b200 as dkv  # noqa: E402
 from paper_2605_15422_b200._lib import lib  # noqa: E402
 
-EV = ["Qld", "Qarr", "iS", "idP", "idV", "idK", "idQ", "cS", "cP", "cdP", "cdS", "dDQ", "dLD", "dEND", "mEND", "x15", "st", "kld"]
+EV = ["Qld", "Qarr", "iS", "idP", "idV", "idK", "idQ", "cS", "cP", "cdP", "cdS", "dDQ", "dLD", "dEND", "mEND", "x15", "kld", "sEND", "sDONE"]
 cta = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 show = int(sys.argv[2]) if len(sys.argv) > 2 else 12
 n, p, r, h, hk, d = 32, 8192, 2048, 32, 8, 128
@@ -29,7 +29,7 @@ run()
 torch.cuda.synchronize()
 fn = getattr(lib, os.environ.get("TRACE_FN", "dkv_trace_read_v1"))
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = np.zeros((18, 256), dtype=np.int64)
+buf = np.zeros((20, 256), dtype=np.int64)
 fn(None, cta)
 run()
 torch.cuda.synchronize()
@@ -42,7 +42,7 @@ for i in range(min(show, 256)):
     if rel[2, i] < 0 and rel[7, i] < 0:
         break
     per = rel[2, i] - rel[2, i - 1] if i > 0 and rel[2, i - 1] >= 0 else 0
-    print(f"{i:4d} " + " ".join(f"{rel[e, i]:7d}" for e in list(range(16)) + [17]) + f"  {per}")
+    print(f"{i:4d} " + " ".join(f"{rel[e, i]:7d}" for e in list(range(16)) + [17, 18, 19]) + f"  {per}")
 valid = [i for i in range(1, 256) if rel[2, i] > 0 and rel[2, i - 1] > 0]
 if valid:
     per = np.diff(rel[2, [0] + valid])

@@ -25,7 +25,7 @@ run()
 torch.cuda.synchronize()
 fn = lib.dkv_trace_read_fwd
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = np.zeros((18, 256), dtype=np.int64)  # kTraceEvents x kTraceTiles (trace.cuh)
+buf = np.zeros((20, 256), dtype=np.int64)  # kTraceEvents x kTraceTiles (trace.cuh)
 fn(None, cta)
 run()
 torch.cuda.synchronize()
