@@ -46,8 +46,14 @@ namespace bwdp {
 constexpr int D = 128;
 constexpr int kBK = 128;            // keys per CTA
 constexpr int kBQ = 64;             // query rows per tile
-constexpr int kThreads = 480;
-constexpr int kWDrain = 8, kWProd = 12, kWMma = 13, kWMma2 = 14;
+#ifndef PAIR_CW
+#define PAIR_CW 8  // compute warps: 8 (32 query columns each) or 16 (16 columns each)
+#endif
+constexpr int kCW = PAIR_CW;
+constexpr int kCC = 256 / kCW;  // query columns per compute warp (4 lane quadrants x 64 columns)
+static_assert(kCW == 8 || kCW == 16, "PAIR_CW: 8 or 16");
+constexpr int kWDrain = kCW, kWProd = kCW + 4, kWMma = kCW + 5, kWMma2 = kCW + 6;
+constexpr int kThreads = (kCW + 7) * 32;
 constexpr int kNSt = 2;  // stages of the query-half operands (S^T / dP^T)
 constexpr int kKSt = 2;  // stages of the head-dim-half operands (dV / dK), needed one tile later
 constexpr int kPanel = kBK * 128;   // 16 KB: one 64-column SW128 panel of a 128-row key tile
@@ -274,13 +280,13 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
   if (threadIdx.x == 0) {
     mbar_init(&bar.kv_full, 1);
     mbar_init(&bar.sdp_full, 1);
-    mbar_init(&bar.sdp_empty, 16);  // 8 compute warps x 2 CTAs
-    mbar_init(&bar.pds_full, 16);   // 8 compute warps x 2 CTAs
+    mbar_init(&bar.sdp_empty, 2 * kCW);  // every compute warp of both CTAs
+    mbar_init(&bar.pds_full, 2 * kCW);
     mbar_init(&bar.p_empty, 1);
     for (int b = 0; b < 2; ++b) {
       // leader: its issuer's expect_tx arrival, the peer forwarder's (the leader's st.async half
       // landed there) and the 4 + 4 warps that store their half locally; peer: its forwarder's
-      mbar_init(&bar.ds_in[b], rank == 0 ? 10 : 1);
+      mbar_init(&bar.ds_in[b], rank == 0 ? 2 + kCW : 1);
       mbar_init(&bar.ds_empty[b], 1);
     }
     mbar_init(&bar.kv_done, 1);
@@ -493,9 +499,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
       }
     }
   } else if (warp < kWDrain) {
-    // ================= compute warps (both CTAs): thread = key row r, 32 query columns per warp
+    // ================= compute warps (both CTAs): thread = key row r, kCC query columns per warp
     const int r = (warp & 3) * 32 + lane;
-    const int c0 = (warp >> 2) * 32;
+    const int c0 = (warp >> 2) * kCC;
     const int qh = c0 >> 5;  // query half of this warp's columns = the CTA whose dQ^T B needs them
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const int key = kbase + r;
@@ -511,9 +517,14 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
       pwait<PAIR_NS_C>(&bar.sdp_full, i & 1);
       tc_fence_after();
       if (threadIdx.x == 0) TRACE(T_C_S, i);
-      uint32_t us[32], ud[32];
-      tmem_ld32(tmem + lane_off + c0, us);
-      tmem_ld32(tmem + lane_off + 64 + c0, ud);
+      uint32_t us[kCC], ud[kCC];
+      if constexpr (kCC == 32) {
+        tmem_ld32(tmem + lane_off + c0, *reinterpret_cast<uint32_t(*)[32]>(us));
+        tmem_ld32(tmem + lane_off + 64 + c0, *reinterpret_cast<uint32_t(*)[32]>(ud));
+      } else {
+        tmem_ld16(tmem + lane_off + c0, *reinterpret_cast<uint32_t(*)[16]>(us));
+        tmem_ld16(tmem + lane_off + 64 + c0, *reinterpret_cast<uint32_t(*)[16]>(ud));
+      }
       tmem_wait_ld();
       if (threadIdx.x == 0) TRACE(T_C_DP, i);
       tc_fence_before();
@@ -527,14 +538,14 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
       }
       const int cmax = min(qrows, (it.rlen - it.tok) * G);
       const float2 sl2 = make_float2(p.scale_log2, p.scale_log2);
-      uint32_t pp[16], pd[16];
+      uint32_t pp[kCC / 2], pd[kCC / 2];
       auto math = [&](auto masked) {
 #pragma unroll
-        for (int c2 = 0; c2 < 16; ++c2) {
+        for (int c2 = 0; c2 < kCC / 2; ++c2) {
           const float2 x =
               __fmul2_rn(make_float2(__uint_as_float(us[2 * c2]), __uint_as_float(us[2 * c2 + 1])), sl2);
           float2 e;
-          if (c2 >= 16 - PAIR_POLY) {
+          if (c2 >= kCC / 2 - PAIR_POLY) {
             e = ex2_poly2(x);  // on the FMA pipe: the math phase is on the compute warps' critical chain
           } else {
             e.x = ex2(x.x);
@@ -551,7 +562,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
           pd[c2] = pack_bf16(dd.x, dd.y);
         }
       };
-      if (__all_sync(0xffffffffu, cmin <= c0 && cmax >= c0 + 32))
+      if (__all_sync(0xffffffffu, cmin <= c0 && cmax >= c0 + kCC))
         math(std::false_type{});
       else
         math(std::true_type{});
@@ -559,8 +570,13 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
       pwait<PAIR_NS_C>(&bar.p_empty, (i & 1) ^ 1);  // dV / dK of tile i - 1 done with P^T / dS^T
       tc_fence_after();
       if (threadIdx.x == 0) TRACE(T_MMA_END, i);
-      tmem_st16(tmem + lane_off + 128 + c0 / 2, pp);
-      tmem_st16(tmem + lane_off + 160 + c0 / 2, pd);
+      if constexpr (kCC == 32) {
+        tmem_st16(tmem + lane_off + 128 + c0 / 2, *reinterpret_cast<const uint32_t(*)[16]>(pp));
+        tmem_st16(tmem + lane_off + 160 + c0 / 2, *reinterpret_cast<const uint32_t(*)[16]>(pd));
+      } else {
+        tmem_st8(tmem + lane_off + 128 + c0 / 2, *reinterpret_cast<const uint32_t(*)[8]>(pp));
+        tmem_st8(tmem + lane_off + 160 + c0 / 2, *reinterpret_cast<const uint32_t(*)[8]>(pd));
+      }
       tmem_wait_st();
       tc_fence_before();
       warp_arrive_leader_relaxed(&bar.pds_full, rank);  // dV / dK of tile i may go
@@ -569,11 +585,12 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
       // the stores and their proxy fence stay off the pds_full -> dV / dK -> p_empty loop
       const int b = i & 1;
       pwait<PAIR_NS_C>(&bar.ds_empty[b], ((i >> 1) & 1) ^ 1);
+      const int ch0 = (c0 & 31) / 8;  // first 16 B chunk of these columns in the 64 B query-half row
       if (ds_here) {
         uint8_t* ds_local = ds_local0 + b * kDSBytes;
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch)
-          *reinterpret_cast<uint4*>(ds_local + sw64_offset(ds_row, ch)) =
+        for (int ch = 0; ch < kCC / 8; ++ch)
+          *reinterpret_cast<uint4*>(ds_local + sw64_offset(ds_row, ch0 + ch)) =
               make_uint4(pd[4 * ch], pd[4 * ch + 1], pd[4 * ch + 2], pd[4 * ch + 3]);
         fence_async_smem();
         warp_arrive_leader_relaxed(&bar.ds_in[b], rank);
@@ -581,9 +598,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
         const uint32_t ds_remote = ds_remote0 + b * kDSBytes;
         const uint32_t ds_rbar = ds_rbar0 + b * 8;  // &ds_in[b] in the peer
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch)
-          st_async_v4(ds_remote + sw64_offset(ds_row, ch), ds_rbar, pd[4 * ch], pd[4 * ch + 1], pd[4 * ch + 2],
-                      pd[4 * ch + 3]);
+        for (int ch = 0; ch < kCC / 8; ++ch)
+          st_async_v4(ds_remote + sw64_offset(ds_row, ch0 + ch), ds_rbar, pd[4 * ch], pd[4 * ch + 1],
+                      pd[4 * ch + 2], pd[4 * ch + 3]);
       }
       if (threadIdx.x == 4 * 32) TRACE(T_EXTRA, i);  // a warp of the other query half
       if (threadIdx.x == 0) TRACE(T_C_DS, i);
