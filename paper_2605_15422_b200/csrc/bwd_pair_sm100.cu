@@ -177,6 +177,9 @@ DKV_DEVICE void warp_arrive_leader_relaxed(uint64_t* bar, uint32_t rank) {
 #ifndef PAIR_NS
 #define PAIR_NS -1
 #endif
+#ifndef PAIR_DS_EARLY
+#define PAIR_DS_EARLY 1  // dS^T operand stores before the P^T / dS^T TMEM stores (C3: 25.91 vs 26.09 ms)
+#endif
 #ifndef PAIR_NS_C
 #define PAIR_NS_C PAIR_NS  // compute warps' waits (S ready, P^T / dS^T buffers free)
 #endif
@@ -437,6 +440,21 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
       const uint32_t id_dq = idesc_bf16_f32(128, kBQ, true, true);
       const uint64_t dKT = sdesc_sw128(smem_u32(base + kOffKT), 0, 1024);
       const uint32_t sDS0 = smem_u32(base + kOffDS);
+      auto issue_dq = [&](int j) {
+        const int b = j & 1;
+        pwait<PAIR_NS_I>(&bar.ds_in[b], (j >> 1) & 1);
+        TRACE(T_ISS_DK, j);
+        pwait<PAIR_NS_I>(&bar.dq_empty[b], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        fence_async_smem();  // the peer's st.async dS^T half -> visible to the tensor core
+        TRACE(T_ISS_DQ, j);
+        const uint64_t dDS = sdesc_sw64(sDS0 + b * kDSBytes);
+#pragma unroll
+        for (int k = 0; k < 2 * kBK / 16; ++k)
+          mma_ss2(tdQ + b * 32, dKT + koff_mn(k), dDS + static_cast<uint64_t>((k * 1024) >> 4), id_dq, k > 0);
+        mma_commit2_mc(&bar.dq_full[b]);
+        mma_commit2_mc(&bar.ds_empty[b]);
+      };
       pwait<PAIR_NS_I>(&bar.kv_full, 0);
       for (int j = 0; j < nq; ++j) {
         const int sj = j % kKSt;
@@ -459,19 +477,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
         mma_commit2_mc(&bar.qk_empty[sj]);
         mma_commit2_mc(&bar.p_empty);
         // dQ^T of tile j: both CTAs' dS^T halves (ds_in: the peer's st.async bytes here + the peer
-        // forwarder's report of the leader's bytes there) and a free dQ^T TMEM buffer
-        pwait<PAIR_NS_I>(&bar.ds_in[b], (j >> 1) & 1);
-        TRACE(T_ISS_DK, j);
-        pwait<PAIR_NS_I>(&bar.dq_empty[b], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        fence_async_smem();  // the peer's st.async dS^T half -> visible to the tensor core
-        TRACE(T_ISS_DQ, j);
-        const uint64_t dDS = sdesc_sw64(sDS0 + b * kDSBytes);
-#pragma unroll
-        for (int k = 0; k < 2 * kBK / 16; ++k)
-          mma_ss2(tdQ + b * 32, dKT + koff_mn(k), dDS + static_cast<uint64_t>((k * 1024) >> 4), id_dq, k > 0);
-        mma_commit2_mc(&bar.dq_full[b]);
-        mma_commit2_mc(&bar.ds_empty[b]);
+        // forwarder's report of the leader's bytes there) and a free dQ^T TMEM buffer.  (Issuing
+        // it one tile later, behind the next dV / dK, measured 28.3 vs 26.7 ms.)
+        issue_dq(j);
       }
       mma_commit2_mc(&bar.kv_done);
 #ifdef DKV_TRACE
@@ -567,6 +575,27 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
       else
         math(std::true_type{});
       if (threadIdx.x == 0) TRACE(T_C_P, i);
+#if PAIR_DS_EARLY
+      // dS^T -> the dQ^T operand first (buffer i % 2, free once dQ^T of tile i - 2 is done), so the
+      // local writers' proxy fence further down finds these stores complete
+      const int b = i & 1;
+      pwait<PAIR_NS_C>(&bar.ds_empty[b], ((i >> 1) & 1) ^ 1);
+      const int ch0 = (c0 & 31) / 8;
+      if (ds_here) {
+        uint8_t* ds_local = ds_local0 + b * kDSBytes;
+#pragma unroll
+        for (int ch = 0; ch < kCC / 8; ++ch)
+          *reinterpret_cast<uint4*>(ds_local + sw64_offset(ds_row, ch0 + ch)) =
+              make_uint4(pd[4 * ch], pd[4 * ch + 1], pd[4 * ch + 2], pd[4 * ch + 3]);
+      } else {
+        const uint32_t ds_remote = ds_remote0 + b * kDSBytes;
+        const uint32_t ds_rbar = ds_rbar0 + b * 8;  // &ds_in[b] in the peer
+#pragma unroll
+        for (int ch = 0; ch < kCC / 8; ++ch)
+          st_async_v4(ds_remote + sw64_offset(ds_row, ch0 + ch), ds_rbar, pd[4 * ch], pd[4 * ch + 1],
+                      pd[4 * ch + 2], pd[4 * ch + 3]);
+      }
+#endif
       pwait<PAIR_NS_C>(&bar.p_empty, (i & 1) ^ 1);  // dV / dK of tile i - 1 done with P^T / dS^T
       tc_fence_after();
       if (threadIdx.x == 0) TRACE(T_MMA_END, i);
@@ -580,6 +609,12 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
       tmem_wait_st();
       tc_fence_before();
       warp_arrive_leader_relaxed(&bar.pds_full, rank);  // dV / dK of tile i may go
+#if PAIR_DS_EARLY
+      if (ds_here) {
+        fence_async_smem();
+        warp_arrive_leader_relaxed(&bar.ds_in[i & 1], rank);
+      }
+#else
       // dS^T (32 query columns of this key) -> buffer i % 2 of the B operand of the CTA owning that
       // query half, once dQ^T of tile i - 2 is done with it; only dQ^T waits for these (ds_in), so
       // the stores and their proxy fence stay off the pds_full -> dV / dK -> p_empty loop
@@ -602,6 +637,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_pair_kernel(const __gr
           st_async_v4(ds_remote + sw64_offset(ds_row, ch0 + ch), ds_rbar, pd[4 * ch], pd[4 * ch + 1],
                       pd[4 * ch + 2], pd[4 * ch + 3]);
       }
+#endif
       if (threadIdx.x == 4 * 32) TRACE(T_EXTRA, i);  // a warp of the other query half
       if (threadIdx.x == 0) TRACE(T_C_DS, i);
     }
