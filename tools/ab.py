@@ -14,6 +14,8 @@ import paper_2605_15422_b200 as dkv  # noqa: E402
 
 reps = int(os.environ.get("AB_REPS", "5"))
 n, p, r, h, hk, d = 32, 8192, 2048, 32, 8, 128
+if os.environ.get("AB_SHAPE"):  # "n,p,r,h,hk" (d = 128), e.g. C5's one group: 32,16384,2048,32,4
+    n, p, r, h, hk = (int(x) for x in os.environ["AB_SHAPE"].split(","))
 g = torch.Generator(device="cuda").manual_seed(0)
 mk = lambda *s: torch.randn(*s, device="cuda", generator=g).to(torch.bfloat16)
 t = n * r
