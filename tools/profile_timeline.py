@@ -5,8 +5,11 @@ import numpy as np, torch
 sys.path.insert(0, os.getcwd())
 import paper_2605_15422_b200 as dkv
 n, p, r, h, hk, d = 32, 8192, 2048, 32, 8, 128
+dt = torch.bfloat16
+if os.environ.get("TL_C1"):  # BASELINE config C1: fp32, N=4 P=256 R=128, 8 heads, d=64
+    n, p, r, h, hk, d, dt = 4, 256, 128, 8, 8, 64, torch.float32
 g = torch.Generator(device="cuda").manual_seed(0)
-mk = lambda *s: torch.randn(*s, device="cuda", generator=g).to(torch.bfloat16)
+mk = lambda *s: torch.randn(*s, device="cuda", generator=g).to(dt)
 t = n * r
 qc, kc, vc, doc = mk(p, h, d), mk(p, hk, d), mk(p, hk, d), mk(p, h, d)
 q, kd, vd, dod = mk(t, h, d), mk(t, hk, d), mk(t, hk, d), mk(t, h, d)
