@@ -79,6 +79,43 @@ static int check_launch(const char* what) {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// SIMT path of the two-call launches: Call 1 (the prompt's self-attention) runs on a side stream
+// forked from and joined back into the caller's stream, so its small latency-bound grids overlap
+// Call 2's (the tensor-core path fuses both into one launch instead).  One side stream and one
+// fork / join event pair per (host thread, device): no state is shared between threads.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideStream* side_stream() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return nullptr;
+  thread_local std::vector<SideStream> cache;
+  if (dev >= static_cast<int>(cache.size())) cache.resize(dev + 1);
+  SideStream& x = cache[dev];
+  if (!x.s) {
+    if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      x = SideStream{};
+      return nullptr;  // fall back to running Call 1 on the caller's stream
+    }
+  }
+  return &x;
+}
+static cudaStream_t fork_side(SideStream* sd, cudaStream_t st) {
+  if (!sd) return st;
+  cudaEventRecord(sd->fork, st);
+  cudaStreamWaitEvent(sd->s, sd->fork, 0);
+  return sd->s;
+}
+static void join_side(SideStream* sd, cudaStream_t st) {
+  if (!sd) return;
+  cudaEventRecord(sd->join, sd->s);
+  cudaStreamWaitEvent(st, sd->join, 0);
+}
+
 template <typename P>
 static int validate_common(const P* p, bool dualkv, const char* fn) {
   if (!p) return fail(DKV_ERR_INVALID, std::string(fn) + ": null params");
@@ -385,6 +422,8 @@ static int bwd_impl(const dkv_bwd_params* p, const CtxSelf* self, void* ws, size
   } else {
     float* drow = reinterpret_cast<float*>(w + L.drow);
     prof_main_begin(1, st);
+    SideStream* sd = with_self && a.total_q > 0 ? side_stream() : nullptr;
+    const cudaStream_t st1 = fork_side(sd, st);  // Call 1 beside Call 2 (disjoint outputs / parts)
     if (a.total_q > 0) {
       launch_rowsum_do_o(a, drow, nullptr, 0, st);
       launch_simt_bwd(a, drow, L.chunk, L.num_chunks, ctx, nullptr, st);
@@ -393,10 +432,11 @@ static int bwd_impl(const dkv_bwd_params* p, const CtxSelf* self, void* ws, size
     if (with_self) {
       // Call 1's prompt-key gradient lands in fp32 as the last part: still one cast in total
       float* drow_s = reinterpret_cast<float*>(w + L.drow_s);
-      launch_rowsum_do_o(s, drow_s, nullptr, 0, st);
-      launch_simt_bwd(s, drow_s, 1, 1, nullptr, ctx + static_cast<int64_t>(L.self_part) * 2 * plane, st);
+      launch_rowsum_do_o(s, drow_s, nullptr, 0, st1);
+      launch_simt_bwd(s, drow_s, 1, 1, nullptr, ctx + static_cast<int64_t>(L.self_part) * 2 * plane, st1);
       prof_count(3);
     }
+    join_side(sd, st);
     prof_main_end(1, st);
   }
   if (plane > 0) {
@@ -502,6 +542,8 @@ int32_t dkv_twocall_fwd(const dkv_twocall_fwd_params* p, void* stream) {
     rc = launch_tc_fwd(a, c->ctx_len > 0 ? &self : nullptr, grp, st);
     if (rc) return rc;
   } else {
+    SideStream* sd = c->ctx_len > 0 && a.total_q > 0 ? side_stream() : nullptr;
+    const cudaStream_t st1 = fork_side(sd, st);  // Call 1 beside Call 2
     if (a.total_q > 0) launch_simt_fwd(a, st);
     if (c->ctx_len > 0) {
       SimtArgs s = a;
@@ -515,8 +557,9 @@ int32_t dkv_twocall_fwd(const dkv_twocall_fwd_params* p, void* stream) {
       s.max_seqlen = s.total_q;
       s.ctx_len = 0;
       s.cu = nullptr;  // one sequence: the prompt
-      launch_simt_fwd(s, st);
+      launch_simt_fwd(s, st1);
     }
+    join_side(sd, st);
   }
   prof_main_end(0, st);
   prof_count(1);
