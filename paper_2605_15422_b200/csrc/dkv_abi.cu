@@ -87,13 +87,19 @@ struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
-static SideStream* side_stream() {
+static SideStream* side_stream(cudaStream_t st) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return nullptr;
-  thread_local std::vector<SideStream> cache;
+  thread_local std::vector<SideStream> cache;  // (created once, kept for the thread's lifetime)
   if (dev >= static_cast<int>(cache.size())) cache.resize(dev + 1);
   SideStream& x = cache[dev];
   if (!x.s) {
+    // never create it inside a stream capture (the fork / join themselves are capture-safe)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return nullptr;
+    }
     if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
@@ -422,7 +428,7 @@ static int bwd_impl(const dkv_bwd_params* p, const CtxSelf* self, void* ws, size
   } else {
     float* drow = reinterpret_cast<float*>(w + L.drow);
     prof_main_begin(1, st);
-    SideStream* sd = with_self && a.total_q > 0 ? side_stream() : nullptr;
+    SideStream* sd = with_self && a.total_q > 0 ? side_stream(st) : nullptr;
     const cudaStream_t st1 = fork_side(sd, st);  // Call 1 beside Call 2 (disjoint outputs / parts)
     if (a.total_q > 0) {
       launch_rowsum_do_o(a, drow, nullptr, 0, st);
@@ -542,7 +548,7 @@ int32_t dkv_twocall_fwd(const dkv_twocall_fwd_params* p, void* stream) {
     rc = launch_tc_fwd(a, c->ctx_len > 0 ? &self : nullptr, grp, st);
     if (rc) return rc;
   } else {
-    SideStream* sd = c->ctx_len > 0 && a.total_q > 0 ? side_stream() : nullptr;
+    SideStream* sd = c->ctx_len > 0 && a.total_q > 0 ? side_stream(st) : nullptr;
     const cudaStream_t st1 = fork_side(sd, st);  // Call 1 beside Call 2
     if (a.total_q > 0) launch_simt_fwd(a, st);
     if (c->ctx_len > 0) {
