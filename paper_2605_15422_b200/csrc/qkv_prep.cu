@@ -16,6 +16,8 @@
 // head's sum of squares is a 16-lane shuffle reduction.  HBM-bound: 2 x 12 KB per row at Qwen3-8B.
 #include "dkv_internal.h"
 
+#include <type_traits>
+
 #include <cmath>
 
 namespace dkv {
@@ -140,14 +142,16 @@ __global__ void __launch_bounds__(kThreads) qkv_prep_fwd_kernel(const PrepArgs a
   }
 }
 
-template <int VPH>
-__global__ void __launch_bounds__(kThreads) qkv_prep_bwd_kernel(const PrepArgs a) {
+// kIter >= ceil(nvec / 256): the per-thread dw accumulators cost 8 registers per slot, so the
+// launch picks the smallest power of two (Qwen3-8B: 768 vectors -> 4; a fixed 8 held the kernel at
+// 119 registers and 2 CTAs per SM, 3.6x the forward's time in tools/profile_layer.py)
+template <int VPH, int kIter>
+__global__ void __launch_bounds__(kThreads, 3) qkv_prep_bwd_kernel(const PrepArgs a) {
   __shared__ float cs[256];
   const int half = a.head_dim / 2;
   const int ht = a.heads + 2 * a.kv_heads;
   const int nvec = ht * VPH;
   const int hq = a.heads, hqk = a.heads + a.kv_heads;
-  constexpr int kIter = 8;  // >= ceil(nvec / 256) for up to 2048 vectors per row
   // per-thread partial dw over every row this CTA visits; the vector index (so the d-slice and
   // the head kind) of a thread's k-th slot is the same in every row
   float dwacc[kIter][8];
@@ -335,12 +339,25 @@ extern "C" int32_t dkv_qkv_prep_bwd(const void* dq, const void* dk, const void* 
     return DKV_ERR_INVALID;
   }
   const int grid = grid_for(rows);
+  const int vph = static_cast<int>(head_dim) / 8;
+  const int iters = static_cast<int>(((heads + 2 * kv_heads) * vph + kThreads - 1) / kThreads);
+  auto launch = [&](auto vph_c) {
+    constexpr int V = decltype(vph_c)::value;
+    if (iters <= 1)
+      qkv_prep_bwd_kernel<V, 1><<<grid, kThreads, 0, st>>>(a);
+    else if (iters <= 2)
+      qkv_prep_bwd_kernel<V, 2><<<grid, kThreads, 0, st>>>(a);
+    else if (iters <= 4)
+      qkv_prep_bwd_kernel<V, 4><<<grid, kThreads, 0, st>>>(a);
+    else
+      qkv_prep_bwd_kernel<V, 8><<<grid, kThreads, 0, st>>>(a);
+  };
   if (a.head_dim == 128)
-    qkv_prep_bwd_kernel<16><<<grid, kThreads, 0, st>>>(a);
+    launch(std::integral_constant<int, 16>{});
   else if (a.head_dim == 64)
-    qkv_prep_bwd_kernel<8><<<grid, kThreads, 0, st>>>(a);
+    launch(std::integral_constant<int, 8>{});
   else
-    qkv_prep_bwd_kernel<32><<<grid, kThreads, 0, st>>>(a);
+    launch(std::integral_constant<int, 32>{});
   prof_count(1);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

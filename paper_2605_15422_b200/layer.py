@@ -41,6 +41,7 @@ class DualKVBatch:
     ctx_rows: torch.Tensor    # [sum P_g] int64 packed rows of the prompts, group order
     resp_rows: torch.Tensor   # [sum R] int64 packed rows of the responses
     inv_perm: torch.Tensor    # [T_dk] int64: row of cat(prompts, responses) holding packed row i
+    perm: torch.Tensor        # [T_dk] int64: its inverse, packed row held at cat(...) row j
     cu_seqlens: torch.Tensor  # [N+1] int32 response offsets over all groups
     max_seqlen: int
     group_seq_cu: List[int]
@@ -68,7 +69,7 @@ class DualKVBatch:
         cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
         t = lambda a, dt=torch.int64: torch.as_tensor(a, dtype=dt, device=device)
         b = DualKVBatch(plan.total_dualkv, t(position_ids(plan, "dualkv")), t(ctx_rows), t(resp_rows), t(inv),
-                        t(cu, torch.int32), int(max(lens)) if lens else 0, gs, gc)
+                        t(order), t(cu, torch.int32), int(max(lens)) if lens else 0, gs, gc)
         plan._dev[key] = b
         return b
 
@@ -129,4 +130,5 @@ class DualKVSelfAttention(torch.nn.Module):
         o, _, _ = torch.ops.dualkv.two_call_split(q, k, v, batch.ctx_rows.shape[0], batch.cu_seqlens,
                                                   batch.max_seqlen, self.scale, batch.group_seq_cu,
                                                   batch.group_ctx_cu)
-        return o.index_select(0, batch.inv_perm).reshape(t, self.h * self.d) @ self.w_o
+        # back to the packed row order (a permutation: gather forward, gather by the inverse backward)
+        return library.permute_rows(o, batch.inv_perm, batch.perm).reshape(t, self.h * self.d) @ self.w_o

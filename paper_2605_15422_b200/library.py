@@ -206,6 +206,38 @@ def rope(x: Tensor, positions: Tensor, base: float = 10000.0) -> Tensor:
     return torch.ops.dualkv.rope(x, positions, float(base), False)
 
 
+# ---------------------------------------------------------------- row permutation
+@torch.library.custom_op("dualkv::permute_rows", mutates_args=(), device_types="cuda")
+def _permute_rows(x: Tensor, idx: Tensor, inv_idx: Tensor) -> Tensor:
+    from .packing import _gather
+    return _gather(x, idx, idx.shape[0])
+
+
+@_permute_rows.register_fake
+def _permute_rows_fake(x, idx, inv_idx):
+    return x.new_empty((idx.shape[0],) + tuple(x.shape[1:]))
+
+
+def _permute_setup(ctx, inputs, output):
+    _, idx, inv_idx = inputs
+    ctx.save_for_backward(idx, inv_idx)
+
+
+def _permute_backward(ctx, dy):
+    idx, inv_idx = ctx.saved_tensors
+    # a permutation's adjoint is the inverse permutation: a gather, not index_select's
+    # index_add_ backward (30 ms per C4 micro-batch pair in tools/profile_layer.py)
+    return torch.ops.dualkv.permute_rows(dy.contiguous(), inv_idx, idx), None, None
+
+
+torch.library.register_autograd("dualkv::permute_rows", _permute_backward, setup_context=_permute_setup)
+
+
+def permute_rows(x: Tensor, idx: Tensor, inv_idx: Tensor) -> Tensor:
+    """out[i] = x[idx[i]] for a permutation `idx` (device int64) with inverse `inv_idx`."""
+    return torch.ops.dualkv.permute_rows(x, idx, inv_idx)
+
+
 # ---------------------------------------------------------------- fused QKV epilogue
 @torch.library.custom_op("dualkv::qkv_prep", mutates_args=(), device_types="cuda")
 def _qkv_prep(qkv: Tensor, q_norm: Optional[Tensor], k_norm: Optional[Tensor], positions: Tensor, dst_rows: Tensor,
