@@ -146,19 +146,21 @@ __global__ void __launch_bounds__(kThreads) qkv_prep_fwd_kernel(const PrepArgs a
 // launch picks the smallest power of two (Qwen3-8B: 768 vectors -> 4; a fixed 8 held the kernel at
 // 119 registers and 2 CTAs per SM, 3.6x the forward's time in tools/profile_layer.py)
 template <int VPH, int kIter>
-__global__ void __launch_bounds__(kThreads, 3) qkv_prep_bwd_kernel(const PrepArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) qkv_prep_bwd_kernel(const PrepArgs a) {
   __shared__ float cs[256];
   const int half = a.head_dim / 2;
   const int ht = a.heads + 2 * a.kv_heads;
   const int nvec = ht * VPH;
   const int hq = a.heads, hqk = a.heads + a.kv_heads;
-  // per-thread partial dw over every row this CTA visits; the vector index (so the d-slice and
-  // the head kind) of a thread's k-th slot is the same in every row
-  float dwacc[kIter][8];
+  // per-thread partial dw over every row this CTA visits: kThreads is a multiple of VPH, so a
+  // thread's d-slice (vector index % VPH) is the same in all its slots -- one accumulator per
+  // head kind (q, k) instead of one per slot
+  static_assert(kThreads % VPH == 0, "a thread keeps one d-slice");
+  float dwacc[2][8];
 #pragma unroll
-  for (int it = 0; it < kIter; ++it)
+  for (int kd = 0; kd < 2; ++kd)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) dwacc[it][j] = 0.f;
+    for (int j = 0; j < 8; ++j) dwacc[kd][j] = 0.f;
   const bool norm = a.wq != nullptr;
   for (int64_t r = blockIdx.x; r < a.rows; r += gridDim.x) {
     const uint4* xsrc = reinterpret_cast<const uint4*>(a.qkv + r * ht * a.head_dim);
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 3) qkv_prep_bwd_kernel(const PrepArg
     __syncthreads();
     row_angles(cs, static_cast<double>(a.pos[r]), a.head_dim, a.log2_base, true);
     __syncthreads();
-#pragma unroll
+#pragma unroll 1
     for (int it = 0; it < kIter; ++it) {
       const int i0 = it * kThreads;
       if (i0 >= nvec) break;
@@ -204,7 +206,10 @@ __global__ void __launch_bounds__(kThreads, 3) qkv_prep_bwd_kernel(const PrepArg
           const float c = rstd * rstd * rstd * xu * inv_d;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            dwacc[it][j] = fmaf(g[j], x[j] * rstd, dwacc[it][j]);  // dw += g * x_hat
+            if (head < hq)
+              dwacc[0][j] = fmaf(g[j], x[j] * rstd, dwacc[0][j]);  // dw += g * x_hat
+            else
+              dwacc[1][j] = fmaf(g[j], x[j] * rstd, dwacc[1][j]);
             g[j] = rstd * wv[j] * g[j] - x[j] * c;
           }
         }
@@ -213,15 +218,20 @@ __global__ void __launch_bounds__(kThreads, 3) qkv_prep_bwd_kernel(const PrepArg
     }
   }
   if (!norm) return;
+  const int sub = threadIdx.x % VPH;
+  bool has_q = false, has_k = false;  // does any of this thread's slots hold a q / k head
 #pragma unroll
   for (int it = 0; it < kIter; ++it) {
     const int i = it * kThreads + threadIdx.x;
-    if (i >= nvec) break;
-    const int head = i / VPH, sub = i % VPH;
-    if (head >= hqk) continue;
-    float* dst = (head < hq ? a.dwq : a.dwk) + sub * 8;
+    if (i < nvec) {
+      has_q |= i / VPH < hq;
+      has_k |= i / VPH >= hq && i / VPH < hqk;
+    }
+  }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) atomicAdd(dst + j, dwacc[it][j]);
+  for (int j = 0; j < 8; ++j) {
+    if (has_q) atomicAdd(a.dwq + sub * 8 + j, dwacc[0][j]);
+    if (has_k) atomicAdd(a.dwk + sub * 8 + j, dwacc[1][j]);
   }
 }
 
