@@ -60,30 +60,37 @@ DKV_DEVICE uint4 pack8(const float (&f)[8]) {
   return v;
 }
 
-// the row's (cos, sin) of the d/2 pair angles, as rope_rows_kernel computes them
-DKV_DEVICE void row_angles(float* cs, double pos, int head_dim, double log2_base, bool inverse) {
-  const int half = head_dim / 2;
-  for (int k = threadIdx.x; k < half; k += blockDim.x) {
-    const double inv_freq = exp2(-2.0 * k / static_cast<double>(head_dim) * log2_base);
-    double ang = pos * inv_freq;
-    ang -= 6.283185307179586 * rint(ang * 0.15915494309189535);  // to [-pi, pi]
-    float sf, cf;
-    sincosf(static_cast<float>(ang), &sf, &cf);
-    cs[k] = cf;
-    cs[half + k] = inverse ? -sf : sf;
+// A thread's vectors all start at the same rotation pair (kThreads is a multiple of VPH, so the
+// d-slice of vector i0 + threadIdx.x is fixed): the 4 pair frequencies once per thread, their
+// (cos, sin) once per row in registers -- the double-precision angle reduction of rope_rows_kernel
+// (aux.cu), without a shared per-row table and the two block barriers per row it needed.
+struct ThreadPairs {
+  double inv_freq[4];
+  __device__ void init(int k0, int head_dim, double log2_base) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) inv_freq[j] = exp2(-2.0 * (k0 + j) / static_cast<double>(head_dim) * log2_base);
+  }
+  __device__ void angles(double pos, bool inverse, float (&c)[4], float (&sn)[4]) const {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double ang = pos * inv_freq[j];
+      ang -= 6.283185307179586 * rint(ang * 0.15915494309189535);  // to [-pi, pi]
+      float sf, cf;
+      sincosf(static_cast<float>(ang), &sf, &cf);
+      c[j] = cf;
+      sn[j] = inverse ? -sf : sf;
+    }
+  }
+};
+DKV_DEVICE void rotate8r(float (&f)[8], const float (&c)[4], const float (&sn)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float e = f[2 * j], o = f[2 * j + 1];
+    f[2 * j] = e * c[j] - o * sn[j];
+    f[2 * j + 1] = e * sn[j] + o * c[j];
   }
 }
 
-// rotate the 4 pairs of one 8-element vector starting at pair k0
-DKV_DEVICE void rotate8(float (&f)[8], const float* cs, int half, int k0) {
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float c = cs[k0 + j], s = cs[half + k0 + j];
-    const float e = f[2 * j], o = f[2 * j + 1];
-    f[2 * j] = e * c - o * s;
-    f[2 * j + 1] = e * s + o * c;
-  }
-}
 
 // sum over the VPH lanes that hold one head (VPH = head_dim / 8, a power of two <= 32)
 template <int VPH>
@@ -96,17 +103,18 @@ DKV_DEVICE float head_sum(float x) {
 // one CTA per row (grid-stride): thread i handles vectors i, i + 256, ... of the row
 template <int VPH>
 __global__ void __launch_bounds__(kThreads) qkv_prep_fwd_kernel(const PrepArgs a) {
-  __shared__ float cs[256];  // head_dim <= 256
+  static_assert(kThreads % VPH == 0, "a thread keeps one d-slice");
   const int half = a.head_dim / 2;
   const int ht = a.heads + 2 * a.kv_heads;
   const int nvec = ht * VPH;
   const int hq = a.heads, hqk = a.heads + a.kv_heads;
+  ThreadPairs tp;
+  tp.init(((threadIdx.x % VPH) * 4) % half, a.head_dim, a.log2_base);
   for (int64_t r = blockIdx.x; r < a.rows; r += gridDim.x) {
     const uint4* src = reinterpret_cast<const uint4*>(a.qkv + r * ht * a.head_dim);
     const int64_t d = a.dst[r];
-    __syncthreads();  // the previous row's angles are no longer read
-    row_angles(cs, static_cast<double>(a.pos[r]), a.head_dim, a.log2_base, false);
-    __syncthreads();
+    float cr[4], sr[4];
+    tp.angles(static_cast<double>(a.pos[r]), false, cr, sr);
     for (int i0 = 0; i0 < nvec; i0 += kThreads) {  // whole warps stay in the loop (shuffles)
       const int i = i0 + threadIdx.x;
       const bool live = i < nvec;
@@ -130,7 +138,7 @@ __global__ void __launch_bounds__(kThreads) qkv_prep_fwd_kernel(const PrepArgs a
         }
       }
       if (!live) continue;
-      if (head < hqk) rotate8(f, cs, half, (sub * 4) % half);
+      if (head < hqk) rotate8r(f, cr, sr);
       const uint4 out = pack8(f);
       if (head < hq)
         reinterpret_cast<uint4*>(a.q + (d * a.heads + head) * a.head_dim)[sub] = out;
@@ -147,11 +155,12 @@ __global__ void __launch_bounds__(kThreads) qkv_prep_fwd_kernel(const PrepArgs a
 // 119 registers and 2 CTAs per SM, 3.6x the forward's time in tools/profile_layer.py)
 template <int VPH, int kIter>
 __global__ void __launch_bounds__(kThreads, 4) qkv_prep_bwd_kernel(const PrepArgs a) {
-  __shared__ float cs[256];
   const int half = a.head_dim / 2;
   const int ht = a.heads + 2 * a.kv_heads;
   const int nvec = ht * VPH;
   const int hq = a.heads, hqk = a.heads + a.kv_heads;
+  ThreadPairs tp;
+  tp.init(((threadIdx.x % VPH) * 4) % half, a.head_dim, a.log2_base);
   // per-thread partial dw over every row this CTA visits: kThreads is a multiple of VPH, so a
   // thread's d-slice (vector index % VPH) is the same in all its slots -- one accumulator per
   // head kind (q, k) instead of one per slot
@@ -166,9 +175,8 @@ __global__ void __launch_bounds__(kThreads, 4) qkv_prep_bwd_kernel(const PrepArg
     const uint4* xsrc = reinterpret_cast<const uint4*>(a.qkv + r * ht * a.head_dim);
     uint4* gdst = reinterpret_cast<uint4*>(a.dqkv + r * ht * a.head_dim);
     const int64_t d = a.dst[r];
-    __syncthreads();
-    row_angles(cs, static_cast<double>(a.pos[r]), a.head_dim, a.log2_base, true);
-    __syncthreads();
+    float cr[4], sr[4];
+    tp.angles(static_cast<double>(a.pos[r]), true, cr, sr);  // the adjoint (inverse) rotation
 #pragma unroll 1
     for (int it = 0; it < kIter; ++it) {
       const int i0 = it * kThreads;
@@ -182,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 4) qkv_prep_bwd_kernel(const PrepArg
                           : head < hqk ? reinterpret_cast<const uint4*>(a.k + (d * a.kv_heads + head - hq) * a.head_dim)
                                        : reinterpret_cast<const uint4*>(a.v + (d * a.kv_heads + head - hqk) * a.head_dim);
         unpack8(gsrc[sub], g);
-        if (head < hqk) rotate8(g, cs, half, (sub * 4) % half);  // the adjoint rotation
+        if (head < hqk) rotate8r(g, cr, sr);  // the adjoint rotation
       }
       const __nv_bfloat16* w = head < hq ? a.wq : (head < hqk ? a.wk : nullptr);
       if (norm) {  // every lane joins the shuffles; only q / k heads use them
