@@ -29,6 +29,8 @@
 #include "trace.cuh"
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 namespace dkv {
 namespace fwd {
@@ -582,6 +584,38 @@ static bool fwd_pairs() {
   return v;
 }
 
+// Can a 2-CTA cluster of the pair forward be resident on this device (queried once per device)?
+// If not -- e.g. a partitioned device -- the single-CTA kernel runs instead.
+static bool pair_launchable() {
+  static std::mutex mu;
+  static std::map<int, bool> ok;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = ok.find(dev);
+  if (it != ok.end()) return it->second;
+  const void* fn = reinterpret_cast<const void*>(dualkv_fwd_kernel<128, true>);
+  bool yes = false;
+  if (ensure_smem_optin(fn, Cfg<128>::kSmemBytesPair, "dualkv_fwd_kernel(pair)")) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg<128>::kSmemBytesPair;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    yes = cudaOccupancyMaxActiveClusters(&n, fn, &cfg) == cudaSuccess && n > 0;
+  }
+  cudaGetLastError();
+  ok[dev] = yes;
+  return yes;
+}
+
 template <int D>
 int launch(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, cudaStream_t st) {
   using C = Cfg<D>;
@@ -603,7 +637,7 @@ int launch(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, cudaSt
       return DKV_ERR_CUDA;
     }
   }
-  const bool pair = D == 128 && fwd_pairs() && tq * G == kBM;  // pair mode: full tiles only
+  const bool pair = D == 128 && fwd_pairs() && tq * G == kBM && pair_launchable();  // full tiles only
   if (pair && ((a.total_q > 0 && !make_map_3d_bf16(&p.tm_k64, a.k, a.total_q, a.kv_heads, D, 1, 64)) ||
                (a.ctx_len > 0 && !make_map_3d_bf16(&p.tm_kc64, a.k_ctx, a.ctx_len, a.kv_heads, D, 1, 64)))) {
     set_error("cuTensorMapEncodeTiled failed for the pair-mode K maps");
