@@ -51,6 +51,12 @@ constexpr int kPolyPairs = FWD_POLY;       // of every 16 exponential pairs, on 
 #ifndef FWD_SPIN
 #define FWD_SPIN 0
 #endif
+#ifndef FWD_QT_SPLIT
+// Q-in-TMEM mode: 1 two warps per row (32 keys each, partial maxima exchanged), 0 one warp per
+// row over all 64 keys of the tile (the other eight softmax warps idle).  C3 forward, interleaved
+// x3: 0 is 8.6-9.1 ms, 1 is 9.4-9.8 ms (pair default, 128-key tiles: 8.3-8.5 ms)
+#define FWD_QT_SPLIT 0
+#endif
 #ifndef FWD_ORDER
 // main work-item order: 0 kv head fastest, then sequence, then q block; 1 q block fastest within
 // (sequence, kv head).  A/B at C3 (tools/ab.sh, profiles/r2_ab.md): 1 + evict-normal own K/V is
@@ -73,12 +79,21 @@ struct Cfg {
   static constexpr int kPairStages = 4;
   static constexpr int kSmemTilesPair = 2 * kTileBytes + kPairStages * (kKHalf + kVHalf);
   static constexpr int kSmemBytesPair = kSmemTilesPair + 8192 + 1024;
+  // Q-in-TMEM pair mode (kQT, D = 128): 64-key KV tiles, so S_A / S_B take 64 TMEM columns each and
+  // Q_A / Q_B fit beside them as the S MMA's A operand (TS-MMA: no Q reads from shared memory);
+  // each CTA holds 32 keys of every K tile and 64 d columns of every V tile
+  static constexpr int kKHalfQT = 32 * D * 2;
+  static constexpr int kVHalfQT = 64 * 64 * 2;
+  static constexpr int kQTStages = 8;
+  static constexpr int kSmemTilesQT = 2 * kTileBytes + kQTStages * (kKHalfQT + kVHalfQT);
+  static constexpr int kSmemBytesQT = kSmemTilesQT + 8192 + 1024;
 };
 
 struct Params {
   CUtensorMap tm_q, tm_k, tm_v, tm_kc, tm_vc;
   CUtensorMap tm_qs;      // fused Call 1: the prompt's own queries [P, H, d]
   CUtensorMap tm_k64, tm_kc64;  // pair mode: K boxes of 64 keys (each CTA loads one half)
+  CUtensorMap tm_k32, tm_kc32, tm_v64, tm_vc64;  // Q-in-TMEM pair mode: 32-key K, 64-key V boxes
   __nv_bfloat16* out;
   float* lse;
   __nv_bfloat16* out_s;   // fused Call 1 outputs [P, H, d], lse [H, P]
@@ -94,8 +109,9 @@ struct Params {
 
 struct Smem {
   uint64_t q_full;
-  uint64_t k_full[4], k_empty[4], v_full[4], v_empty[4];
+  uint64_t k_full[8], k_empty[8], v_full[8], v_empty[8];
   uint64_t s_full[2], p_full[2], o_full[2];
+  uint64_t q_tm[2];       // kQT: Q tile t is in TMEM (one arrival per softmax warp of both CTAs)
   uint32_t tmem_base;
   // the two column halves of a row exchange partial row maxima (and, at the end, row sums)
   float xch[2][2][2][128];  // [tile][iteration parity][column half][row]
@@ -105,19 +121,24 @@ struct Smem {
 // the leader (cta_group::2): each CTA loads only half of every K tile (64 keys) and half of
 // every V tile (64 d columns), so K/V traffic into the SMs and the B-operand shared-memory
 // reads per FLOP halve; S, P and O stay in each CTA's own tensor memory.
-template <int D, bool kPair>
+template <int D, bool kPair, bool kQT = false>
 __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
   static_assert(!kPair || D == 128, "pair mode is laid out for d = 128");
-  constexpr int kSt = kPair ? C::kPairStages : C::kStages;
-  constexpr int kKBytes = kPair ? C::kKHalf : C::kTileBytes;  // per K stage
-  constexpr int kVBytes = kPair ? C::kVHalf : C::kTileBytes;  // per V stage
+  static_assert(!kQT || kPair, "Q-in-TMEM is a pair-mode layout");
+  constexpr int BN = kQT ? 64 : kBN;  // keys per KV tile
+  constexpr bool kSplit = !kQT || FWD_QT_SPLIT;  // two softmax warps per row (column halves)
+  constexpr int kHW = kSplit ? BN / 2 : BN;       // keys per softmax thread
+  constexpr int kArr = kSplit ? 16 : 8;           // pair: softmax-warp arrivals (both CTAs) per tile
+  constexpr int kSt = kQT ? C::kQTStages : kPair ? C::kPairStages : C::kStages;
+  constexpr int kKBytes = kQT ? C::kKHalfQT : kPair ? C::kKHalf : C::kTileBytes;  // per K stage
+  constexpr int kVBytes = kQT ? C::kVHalfQT : kPair ? C::kVHalf : C::kTileBytes;  // per V stage
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ[2] = {base, base + C::kTileBytes};
   uint8_t* sK = base + 2 * C::kTileBytes;
   uint8_t* sV = sK + kSt * kKBytes;
-  Smem& sm = *reinterpret_cast<Smem*>(base + (kPair ? C::kSmemTilesPair : C::kSmemTiles));
+  Smem& sm = *reinterpret_cast<Smem*>(base + (kQT ? C::kSmemTilesQT : kPair ? C::kSmemTilesPair : C::kSmemTiles));
   const uint32_t crank = kPair ? cluster_ctarank() : 0;  // 0: the pair's leader (issues the MMAs)
   const int item = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
 
@@ -151,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     const int g = p.grp.group_of(seq);
     ctx_row0 = p.grp.ctx[g];
     ctx_len = p.grp.ctx[g + 1] - ctx_row0;
-    n_ctx = (ctx_len + kBN - 1) / kBN;
+    n_ctx = (ctx_len + BN - 1) / BN;
     mq = &p.tm_q;
     mk_own = &p.tm_k;
     mv_own = &p.tm_v;
@@ -183,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
   // sequence end are computed on zero / foreign rows and never stored
   const bool has_b = kPair || tok0 + p.tq < rlen;
   const int last_tok = min(tok_item + span_tok, rlen) - 1;  // the item's walk: the whole cluster
-  const int n_own = last_tok / kBN + 1;
+  const int n_own = last_tok / BN + 1;
   const int n_iter = n_own + n_ctx;
 
   const int warp = warp_id();
@@ -199,8 +220,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.s_full[i], 1);
-      mbar_init(&sm.p_full[i], kPair ? 16 : 256);  // pair: one arrival per softmax warp of both CTAs
+      mbar_init(&sm.p_full[i], kPair ? kArr : 256);  // pair: one arrival per softmax warp of both CTAs
       mbar_init(&sm.o_full[i], 1);
+      mbar_init(&sm.q_tm[i], kArr);
     }
     fence_mbar_init();
   }
@@ -249,7 +271,13 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
       }
       const uint64_t pol_kv = policy_evict_last();
       const uint64_t pol_own = FWD_EVICT == 1 ? policy_evict_normal() : policy_evict_first();
-      if constexpr (kPair) {
+      if constexpr (kQT) {
+        // Q is read only by this CTA's own threads (copied into TMEM): a local 1-SM load
+        mbar_arrive_expect_tx(&sm.q_full, 2 * C::kTileBytes);
+        for (int t = 0; t < 2; ++t)
+          for (int pn = 0; pn < C::kPanels; ++pn)
+            tma_load_3d(sQ[t] + pn * C::kPanelBytes, mq, &sm.q_full, pn * 64, hk * p.group, seq0 + tok0 + t * p.tq);
+      } else if constexpr (kPair) {
         if (crank == 0) mbar_arrive_expect_tx(&sm.q_full, 4 * C::kTileBytes);
         const uint32_t lq = mapa_shared(&sm.q_full, 0);
         for (int t = 0; t < 2; ++t)
@@ -271,21 +299,23 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         const uint32_t ph = (it / kSt) & 1;
         const CUtensorMap* mk = is_ctx ? &p.tm_kc : mk_own;
         const CUtensorMap* mv = is_ctx ? &p.tm_vc : mv_own;
-        const int row = is_ctx ? ctx_row0 + j * kBN : seq0 + j * kBN;
+        const int row = is_ctx ? ctx_row0 + j * BN : seq0 + j * BN;
         mbar_wait(&sm.k_empty[slot], ph ^ 1);
         TRACE(T_Q_LOAD, it);
         if constexpr (kPair) {
           // this CTA's halves: keys [64 r, +64) of K, d columns [64 r, +64) of V; both counted
           // on the leader's barriers
-          const CUtensorMap* mk64 = is_ctx ? &p.tm_kc64 : (self_item ? &p.tm_kc64 : &p.tm_k64);
-          if (crank == 0) mbar_arrive_expect_tx(&sm.k_full[slot], 2 * C::kKHalf);
+          const bool ctx_map = is_ctx || self_item;
+          const CUtensorMap* mkh = kQT ? (ctx_map ? &p.tm_kc32 : &p.tm_k32) : (ctx_map ? &p.tm_kc64 : &p.tm_k64);
+          const CUtensorMap* mvh = kQT ? (ctx_map ? &p.tm_vc64 : &p.tm_v64) : mv;
+          if (crank == 0) mbar_arrive_expect_tx(&sm.k_full[slot], 2 * kKBytes);
           const uint32_t lk = mapa_shared(&sm.k_full[slot], 0);
           for (int pn = 0; pn < C::kPanels; ++pn)
-            tma_load_3d_2sm(sK + slot * C::kKHalf + pn * (C::kKHalf / 2), mk64, lk, pn * 64, hk,
-                            row + static_cast<int>(crank) * 64);
+            tma_load_3d_2sm(sK + slot * kKBytes + pn * (kKBytes / 2), mkh, lk, pn * 64, hk,
+                            row + static_cast<int>(crank) * (BN / 2));
           mbar_wait(&sm.v_empty[slot], ph ^ 1);
-          if (crank == 0) mbar_arrive_expect_tx(&sm.v_full[slot], 2 * C::kVHalf);
-          tma_load_3d_2sm(sV + slot * C::kVHalf, mv, mapa_shared(&sm.v_full[slot], 0), static_cast<int>(crank) * 64,
+          if (crank == 0) mbar_arrive_expect_tx(&sm.v_full[slot], 2 * kVBytes);
+          tma_load_3d_2sm(sV + slot * kVBytes, mvh, mapa_shared(&sm.v_full[slot], 0), static_cast<int>(crank) * 64,
                           hk, row);
           continue;
         }
@@ -320,9 +350,10 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     // ================= MMA issuer (one thread)
     if ((!kPair || crank == 0) && elect_one()) {
       constexpr int kM = kPair ? 2 * kBM : kBM;
-      const uint32_t idesc_s = idesc_bf16_f32(kM, kBN, false, false);
+      const uint32_t idesc_s = idesc_bf16_f32(kM, BN, false, false);
       const uint32_t idesc_o = idesc_bf16_f32(kM, D, false, true);
-      const uint32_t tS[2] = {tmem + 0, tmem + 128};
+      const uint32_t tS[2] = {tmem + 0, tmem + BN};
+      const uint32_t tQ[2] = {tmem + 128, tmem + 192};  // kQT only
       const uint32_t tO[2] = {tmem + 256, tmem + 256 + 128};
       const int ntile = has_b ? 2 : 1;
       auto issue_s = [&](int t, int kslot) {
@@ -332,8 +363,14 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * C::kPanelBytes + (k & 3) * 32;
           if constexpr (kPair) {
-            const uint32_t koff = (k >> 2) * (C::kKHalf / 2) + (k & 3) * 32;  // 64-row K panels
-            mma_ss2(tS[t], sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + koff, 16, 1024), idesc_s, k > 0);
+            const uint32_t koff = (k >> 2) * (kKBytes / 2) + (k & 3) * 32;  // (BN / 2)-row K panels
+            if constexpr (kQT)
+              mma_ts2(tS[t], tQ[t] + k * 8, sdesc_sw128(ka + koff, 16, 1024), idesc_s, k > 0);
+            else if (DKV_ABL(p.ablate) & 8)  // energy experiment (trace build): A from TMEM (the O
+              // columns, garbage values) -- the S MMA without its Q shared-memory reads
+              mma_ts2(tS[t], tO[t] + k * 8, sdesc_sw128(ka + koff, 16, 1024), idesc_s, k > 0);
+            else
+              mma_ss2(tS[t], sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + koff, 16, 1024), idesc_s, k > 0);
           } else {
             mma_ss(tS[t], sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + off, 16, 1024), idesc_s, k > 0);
           }
@@ -342,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
       auto issue_pv = [&](int t, int vslot, bool accum) {
         const uint32_t va = smem_u32(sV + vslot * kVBytes);
 #pragma unroll
-        for (int k = 0; k < kBN / 16; ++k) {
+        for (int k = 0; k < BN / 16; ++k) {
           if constexpr (kPair)
             mma_ts2(tO[t], tS[t] + k * 8, sdesc_sw128(va + k * 2048, C::kPanelBytes, 1024), idesc_o,
                     (accum || k > 0) ? 1u : 0u);
@@ -369,10 +406,14 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         else
           mbar_wait(bar, ph);
       };
-      wait(&sm.q_full, 0);
+      if constexpr (!kQT) wait(&sm.q_full, 0);
       wait(&sm.k_full[0], 0);
       tc_fence_after();
       for (int t = 0; t < ntile; ++t) {
+        if constexpr (kQT) {
+          wait(&sm.q_tm[t], 0);  // both CTAs' softmax warps copied Q tile t into TMEM
+          tc_fence_after();
+        }
         issue_s(t, 0);
         commit(&sm.s_full[t]);
       }
@@ -416,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     const int row = q * 32 + lane;
     const int bar_id = 1 + t * 4 + q;  // the two warps (h = 0, 1) of this row quadrant
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    const uint32_t tS = tmem + lane_off + t * 128;
+    const uint32_t tS = tmem + lane_off + t * BN;
     const uint32_t tO = tmem + lane_off + 256 + t * 128;
     const bool tile_ok = (t == 0) || has_b;
     const int qtok = tok0 + t * p.tq + row / p.group;  // sequence-local token of this row
@@ -425,9 +466,42 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
     // heads; its last 128 - tq G rows are padding (stale smem rows, computed, never stored)
     const bool row_valid = tile_ok && qtok < rlen && row < p.tq * p.group;
     const int qmin = tok0 + t * p.tq;                  // first token of the tile
-    const int cb = 64 * h;                             // first key column of this half
-    constexpr int kDH = D / 2;                         // O columns this half rescales / stores
+    const int hh = kSplit ? h : 0;                     // column half of this warp (0: whole row)
+    const int cb = kHW * hh;                           // first key column of this half
+    constexpr int kDH = kSplit ? D / 2 : D;            // O columns this warp rescales / stores
     float m_run = -INFINITY, l_run = 0.f;
+    if (!kSplit && h == 1) {
+      done();
+      return;
+    }
+    if constexpr (kQT) {
+      // Q tile t -> TMEM (the S MMA's A operand): this thread's row, d columns [64 h, +64) = one
+      // SW128 panel row = 32 columns of bf16 pairs
+      mbar_wait(&sm.q_full, 0);
+#pragma unroll 1
+      for (int pn = kSplit ? h : 0; pn < (kSplit ? h + 1 : 2); ++pn) {
+        const uint8_t* qp = sQ[t] + pn * C::kPanelBytes;
+        uint32_t u[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 v = *reinterpret_cast<const uint4*>(qp + sw128_offset(row, c));
+          u[4 * c] = v.x;
+          u[4 * c + 1] = v.y;
+          u[4 * c + 2] = v.z;
+          u[4 * c + 3] = v.w;
+        }
+        tmem_st32(tmem + lane_off + 128 + t * 64 + pn * 32, u);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (crank == 0)
+          mbar_arrive(&sm.q_tm[t]);
+        else
+          mbar_arrive_remote_relaxed(mapa_shared(&sm.q_tm[t], 0));
+      }
+    }
     if (tile_ok) {
       for (int it = 0; it < n_iter; ++it) {
         bool is_ctx;
@@ -435,24 +509,24 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         mbar_wait(&sm.s_full[t], it & 1);
         tc_fence_after();
         if (threadIdx.x == 0) TRACE(T_C_S, it);
-        float s[64];
+        float s[kHW];
         {
-          uint32_t u[64];
-          tmem_ld32(tS + cb, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
-          tmem_ld32(tS + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
+          uint32_t u[kHW];
+#pragma unroll
+          for (int c = 0; c < kHW; c += 32) tmem_ld32(tS + cb + c, *reinterpret_cast<uint32_t(*)[32]>(&u[c]));
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 64; ++i) s[i] = __uint_as_float(u[i]);
+          for (int i = 0; i < kHW; ++i) s[i] = __uint_as_float(u[i]);
         }
         if (threadIdx.x == 0) TRACE(T_C_DP, it);
         // masks: own tiles on/after the tile's first token are causal; the last
         // context tile may be partial (keys >= P are out of bounds)
-        const int kbase = j * kBN + cb;
-        const bool need_mask = is_ctx ? (kbase + 64 > ctx_len) : (kbase + 63 > qmin);
+        const int kbase = j * BN + cb;
+        const bool need_mask = is_ctx ? (kbase + kHW > ctx_len) : (kbase + kHW - 1 > qmin);
         if (need_mask) {
           const int lim = is_ctx ? ctx_len - 1 - kbase : qtok - kbase;  // last visible column
 #pragma unroll
-          for (int c = 0; c < 64; ++c)
+          for (int c = 0; c < kHW; ++c)
             if (c > lim) s[c] = -INFINITY;
         }
         // partial row max (8 independent FMNMX3 chains), then the other half's through smem
@@ -460,15 +534,17 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
 #pragma unroll
         for (int i = 0; i < 8; ++i) m8[i] = fmax3(s[i], s[8 + i], s[16 + i]);
 #pragma unroll
-        for (int c = 24; c < 56; c += 16)
+        for (int c = 24; c < kHW - 8; c += 16)
 #pragma unroll
           for (int i = 0; i < 8; ++i) m8[i] = fmax3(m8[i], s[c + i], s[c + 8 + i]);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) m8[i] = fmaxf(m8[i], s[56 + i]);
+        for (int i = 0; i < 8; ++i) m8[i] = fmaxf(m8[i], s[kHW - 8 + i]);
         float mx = fmaxf(fmax3(m8[0], m8[1], m8[2]), fmax3(fmax3(m8[3], m8[4], m8[5]), m8[6], m8[7]));
-        sm.xch[t][it & 1][h][row] = mx;
-        named_bar_sync(bar_id, 64);  // also: both halves' S loads are done before P overwrites S
-        mx = fmaxf(mx, sm.xch[t][it & 1][h ^ 1][row]);
+        if constexpr (kSplit) {
+          sm.xch[t][it & 1][h][row] = mx;
+          named_bar_sync(bar_id, 64);  // also: both halves' S loads are done before P overwrites S
+          mx = fmaxf(mx, sm.xch[t][it & 1][h ^ 1][row]);
+        }
         if (threadIdx.x == 0) TRACE(T_ISS_DQ, it);
         const float m_tile = mx * p.scale_log2;
         const float m_new = fmaxf(m_run, m_tile);
@@ -484,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         const float2 nm2 = make_float2(-m_use, -m_use);
         float2 rs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
+        for (int c0 = 0; c0 < kHW; c0 += 32) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -509,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         // rescales its D/2 columns
         if (it > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-          for (int c0 = h * kDH; c0 < (h + 1) * kDH; c0 += 32) {
+          for (int c0 = hh * kDH; c0 < (hh + 1) * kDH; c0 += 32) {
             uint32_t r[32];
             tmem_ld32(tO + c0, r);
             tmem_wait_ld();
@@ -541,15 +617,17 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_fwd_kernel(const __grid_co
         if (threadIdx.x == 7 * 32) TRACE(T_D_END, it);  // the tile's last softmax warp (trace only)
       }
       // ---- epilogue: l = both halves' partial sums; O / l -> bf16 (each half D/2 columns), lse
-      sm.xch[t][n_iter & 1][h][row] = l_run;
-      named_bar_sync(bar_id, 64);
-      l_run += sm.xch[t][n_iter & 1][h ^ 1][row];
+      if constexpr (kSplit) {
+        sm.xch[t][n_iter & 1][h][row] = l_run;
+        named_bar_sync(bar_id, 64);
+        l_run += sm.xch[t][n_iter & 1][h ^ 1][row];
+      }
       mbar_wait(&sm.o_full[t], 0);
       tc_fence_after();
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
       __nv_bfloat16* orow = out + (static_cast<int64_t>(seq0 + qtok) * p.heads + head) * D;
 #pragma unroll 1
-      for (int c0 = h * kDH; c0 < (h + 1) * kDH; c0 += 32) {
+      for (int c0 = hh * kDH; c0 < (hh + 1) * kDH; c0 += 32) {
         uint32_t r[32];
         tmem_ld32(tO + c0, r);
         tmem_wait_ld();
@@ -584,23 +662,39 @@ static bool fwd_pairs() {
   return v;
 }
 
+// Q as a TMEM operand with 64-key KV tiles (kQT) in the pair forward: DKV_FWD_QT=1.
+static bool fwd_qt() {
+  static const bool v = [] {
+    const char* e = getenv("DKV_FWD_QT");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
+static const void* pair_fn(bool qt) {
+  return qt ? reinterpret_cast<const void*>(dualkv_fwd_kernel<128, true, true>)
+            : reinterpret_cast<const void*>(dualkv_fwd_kernel<128, true, false>);
+}
+static int pair_smem(bool qt) { return qt ? Cfg<128>::kSmemBytesQT : Cfg<128>::kSmemBytesPair; }
+
 // Can a 2-CTA cluster of the pair forward be resident on this device (queried once per device)?
 // If not -- e.g. a partitioned device -- the single-CTA kernel runs instead.
-static bool pair_launchable() {
+static bool pair_launchable(bool qt) {
   static std::mutex mu;
   static std::map<int, bool> ok;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
   std::lock_guard<std::mutex> lock(mu);
-  auto it = ok.find(dev);
+  const int key = 2 * dev + (qt ? 1 : 0);
+  auto it = ok.find(key);
   if (it != ok.end()) return it->second;
-  const void* fn = reinterpret_cast<const void*>(dualkv_fwd_kernel<128, true>);
+  const void* fn = pair_fn(qt);
   bool yes = false;
-  if (ensure_smem_optin(fn, Cfg<128>::kSmemBytesPair, "dualkv_fwd_kernel(pair)")) {
+  if (ensure_smem_optin(fn, pair_smem(qt), "dualkv_fwd_kernel(pair)")) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = Cfg<128>::kSmemBytesPair;
+    cfg.dynamicSmemBytes = pair_smem(qt);
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
@@ -612,7 +706,7 @@ static bool pair_launchable() {
     yes = cudaOccupancyMaxActiveClusters(&n, fn, &cfg) == cudaSuccess && n > 0;
   }
   cudaGetLastError();
-  ok[dev] = yes;
+  ok[key] = yes;
   return yes;
 }
 
@@ -637,10 +731,19 @@ int launch(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, cudaSt
       return DKV_ERR_CUDA;
     }
   }
-  const bool pair = D == 128 && fwd_pairs() && tq * G == kBM && pair_launchable();  // full tiles only
+  const bool qt = D == 128 && fwd_qt();
+  const bool pair = D == 128 && fwd_pairs() && tq * G == kBM && pair_launchable(qt);  // full tiles only
   if (pair && ((a.total_q > 0 && !make_map_3d_bf16(&p.tm_k64, a.k, a.total_q, a.kv_heads, D, 1, 64)) ||
                (a.ctx_len > 0 && !make_map_3d_bf16(&p.tm_kc64, a.k_ctx, a.ctx_len, a.kv_heads, D, 1, 64)))) {
     set_error("cuTensorMapEncodeTiled failed for the pair-mode K maps");
+    return DKV_ERR_CUDA;
+  }
+  if (pair && qt &&
+      ((a.total_q > 0 && (!make_map_3d_bf16(&p.tm_k32, a.k, a.total_q, a.kv_heads, D, 1, 32) ||
+                          !make_map_3d_bf16(&p.tm_v64, a.v, a.total_q, a.kv_heads, D, 1, 64))) ||
+       (a.ctx_len > 0 && (!make_map_3d_bf16(&p.tm_kc32, a.k_ctx, a.ctx_len, a.kv_heads, D, 1, 32) ||
+                          !make_map_3d_bf16(&p.tm_vc64, a.v_ctx, a.ctx_len, a.kv_heads, D, 1, 64))))) {
+    set_error("cuTensorMapEncodeTiled failed for the Q-in-TMEM K/V maps");
     return DKV_ERR_CUDA;
   }
   const bool with_self = self && a.ctx_len > 0;
@@ -681,12 +784,11 @@ int launch(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, cudaSt
   p.n_main_items = static_cast<int>(main_items);
   p.blocks_per_seq = blocks_per_seq;
   if (pair) {
-    const void* fn = reinterpret_cast<const void*>(dualkv_fwd_kernel<128, true>);
-    if (!ensure_smem_optin(fn, C::kSmemBytesPair, "dualkv_fwd_kernel(pair)")) return DKV_ERR_CUDA;
+    if (!ensure_smem_optin(pair_fn(qt), pair_smem(qt), "dualkv_fwd_kernel(pair)")) return DKV_ERR_CUDA;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(2 * items));
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = C::kSmemBytesPair;
+    cfg.dynamicSmemBytes = pair_smem(qt);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -695,7 +797,8 @@ int launch(const SimtArgs& a, const CtxSelf* self, const GroupTable& grp, cudaSt
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, dualkv_fwd_kernel<128, true>, p);
+    const cudaError_t e = qt ? cudaLaunchKernelEx(&cfg, dualkv_fwd_kernel<128, true, true>, p)
+                             : cudaLaunchKernelEx(&cfg, dualkv_fwd_kernel<128, true, false>, p);
     if (e != cudaSuccess) {
       set_error(std::string("forward pair launch failed: ") + cudaGetErrorString(e));
       return DKV_ERR_CUDA;

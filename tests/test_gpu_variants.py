@@ -46,12 +46,16 @@ def _run(tmp_path, name, env_extra, h, hk):
 
 
 # each switch flips one CTA-pair (cta_group::2) kernel against its single-CTA counterpart:
-# the forward pair is the default (DKV_FWD_PAIR=0 turns it off), the backward pair is opt-in
+# the forward pair is the default (DKV_FWD_PAIR=0 turns it off), the backward pair is opt-in;
+# DKV_FWD_QT is the pair forward with Q as a TMEM operand and 64-key KV tiles (opt-in)
 @pytest.mark.parametrize("switch,h,hk", [("DKV_FWD_PAIR", 16, 4), ("DKV_FWD_PAIR", 32, 4), ("DKV_BWD_PAIR", 16, 4),
-                                         ("DKV_BWD_PAIR", 8, 8), ("DKV_BWD_PAIR", 32, 4), ("DKV_BWD_PAIR", 32, 2)])
+                                         ("DKV_BWD_PAIR", 8, 8), ("DKV_BWD_PAIR", 32, 4), ("DKV_BWD_PAIR", 32, 2),
+                                         ("DKV_FWD_PAIR+DKV_FWD_QT", 16, 4), ("DKV_FWD_PAIR+DKV_FWD_QT", 32, 4),
+                                         ("DKV_FWD_PAIR+DKV_FWD_QT", 8, 8)])
 def test_variant_matches_default(switch, h, hk, tmp_path, cuda_device):
     base = _run(tmp_path, "single", {"DKV_FWD_PAIR": "0", "DKV_BWD_PAIR": "0"}, h, hk)
-    var = _run(tmp_path, switch, {"DKV_FWD_PAIR": "0", "DKV_BWD_PAIR": "0", switch: "1"}, h, hk)
+    var = _run(tmp_path, switch, {"DKV_FWD_PAIR": "0", "DKV_BWD_PAIR": "0", **{s: "1" for s in switch.split("+")}},
+               h, hk)
     for k, ref in base.items():
         got = var[k]
         tol = 1e-3 if k.startswith("l") else 2e-2

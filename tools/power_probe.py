@@ -42,6 +42,6 @@ torch.cuda.synchronize()
 stop.set(); th.join()
 s = np.array([x[:2] for x in samples[len(samples) // 5:]])
 reasons = set(x[2] for x in samples)
-print(f"{which} ablate={os.environ.get('DKV_BWD_ABLATE', '0')} ms={e0.elapsed_time(e1) / reps:.3f} "
+print(f"{which} ablate={os.environ.get('DKV_BWD_ABLATE', '0')}/{os.environ.get('DKV_FWD_ABLATE', '0')} ms={e0.elapsed_time(e1) / reps:.3f} "
       f"sm_mhz median={np.median(s[:, 0]):.0f} min={s[:, 0].min():.0f} power_w median={np.median(s[:, 1]):.0f} "
       f"max={s[:, 1].max():.0f} reasons={sorted(hex(x) for x in reasons)} n={len(s)}")
