@@ -376,11 +376,21 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
           const uint64_t dX = sdesc_sw32(smem_u32(base + kOffX + st * 2 * kXBytes));
           TRACE(T_ISS_S, i);
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) mma_ss(tS, dKk + koff_kv(k), dQk + koff_q(k), id_sdp, k > 0);
+          for (int k = 0; k < D / 16; ++k) {
+            if (DKV_ABL(p.ablate) & 16)  // energy experiment (trace build): A from TMEM (dV columns,
+              mma_ts(tS, tdV + k * 8, dQk + koff_q(k), id_sdp, k > 0);  // garbage): no K smem reads
+            else
+              mma_ss(tS, dKk + koff_kv(k), dQk + koff_q(k), id_sdp, k > 0);
+          }
           // S^T[k][c] += -lse[c] / scale  (so that P = exp2(S'^T * scale * log2 e))
           if (!(DKV_ABL(p.ablate) & 8)) mma_ss(tS, dOnes, dX, id_sdp, 1u);
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) mma_ss(tdP, dVk + koff_kv(k), dOk + koff_q(k), id_sdp, k > 0);
+          for (int k = 0; k < D / 16; ++k) {
+            if (DKV_ABL(p.ablate) & 16)
+              mma_ts(tdP, tdK + k * 8, dOk + koff_q(k), id_sdp, k > 0);
+            else
+              mma_ss(tdP, dVk + koff_kv(k), dOk + koff_q(k), id_sdp, k > 0);
+          }
           // dP^T[k][c] += -D[c]  (so that dS^T = P^T * dP'^T)
           if (!(DKV_ABL(p.ablate) & 8)) mma_ss(tdP, dOnes, dX + (kXBytes >> 4), id_sdp, 1u);
           mma_commit(&bar.sdp_full);
