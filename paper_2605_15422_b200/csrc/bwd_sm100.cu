@@ -62,6 +62,12 @@ constexpr int kPolyPairs = BWD_POLY;    // of every 16 exponential pairs, on the
 // backward (108 -> 71 ms) and 5 % on the DualKV backward (its own-response items)
 #define BWD_OWN_ORDER 1
 #endif
+#ifndef BWD_KT
+// 1: K as a TMEM operand of S^T (d = 128): P^T / dS^T aliased onto the S^T / dP^T columns they
+// are computed from, which frees TMEM [128,192) for K; the compute warps report P^T and dS^T
+// separately so dV(i) + S^T(i+1) run while they finish dS^T(i) (profiles/r2_energy_ceilings.md)
+#define BWD_KT 0
+#endif
 constexpr int kStages = 3;
 constexpr int kKVPanel = kBK * 128;         // 16 KB: one 64-column SW128 panel of a key tile
 constexpr int kPBytes = kBK * kBQ * 2;      // 16 KB
@@ -114,6 +120,7 @@ struct Params {
 
 struct Bars {
   uint64_t kv_full, sdp_full, sdp_empty, pds_full, pds_empty, kv_done;
+  uint64_t k_tm, p_ready, dp_full;  // BWD_KT: K in TMEM; P^T(i) stored; dP^T(i) complete
   uint64_t q_full[kStages], q_empty[kStages];
   uint64_t dq_full, dq_empty;
   uint32_t tmem_base;
@@ -157,6 +164,7 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_constant__ Params p) {
   using Y = L<D>;
+  constexpr bool kKT = BWD_KT && D == 128;
   constexpr int kQBytes = Y::kQBytes, kQPanel = Y::kQPanel, kStageBytes = Y::kStageBytes;
   constexpr int kOffK = Y::kOffK, kOffV = Y::kOffV, kOffQ = Y::kOffQ, kOffDO = Y::kOffDO, kOffDS = Y::kOffDS;
   constexpr int kOffX = Y::kOffX, kOffOnes = Y::kOffOnes, kOffStage = Y::kOffStage, kOffBar = Y::kOffBar;
@@ -257,6 +265,9 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     }
     mbar_init(&bar.dq_full, 1);
     mbar_init(&bar.dq_empty, 128);
+    mbar_init(&bar.k_tm, 256);
+    mbar_init(&bar.p_ready, 256);
+    mbar_init(&bar.dp_full, 1);
     fence_mbar_init();
   }
   if (warp == kWProd) tmem_alloc<512>(&bar.tmem_base);
@@ -365,7 +376,67 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
           mbar_wait(b, ph);
       };
       issuer_wait(&bar.kv_full, 0);
-      for (int i = 0; i <= nq; ++i) {
+      if constexpr (kKT) {
+        // S^T = K Q^T with A = K from TMEM [128,192); P^T lives in S^T's columns [16,48) and dS^T in
+        // dP^T's [80,112) (each compute warp's packed columns land on its own fp32 columns).  Per
+        // step i: dV(i-1) -> S^T(i) once P^T(i-1) is stored (the in-order tensor pipe reads P^T
+        // before S^T(i) overwrites it); dK(i-1) -> dP^T(i) once dS^T(i-1) is; then dQ^T(i-1).
+        const uint32_t tK = tmem + 128, tPa = tS + 16, tDSa = tdP + 16;
+        issuer_wait(&bar.k_tm, 0);
+        tc_fence_after();
+        for (int i = 0; i <= nq; ++i) {
+          const int st = i % kStages;
+          const int j = i - 1, sj = (i + kStages - 1) % kStages;
+          if (i > 0) {
+            issuer_wait(&bar.p_ready, j & 1);
+            tc_fence_after();
+            const uint64_t dOm = sdesc_sw128(smem_u32(base + kOffDO + sj * kQBytes), kQPanel, 1024);
+            TRACE(T_ISS_DV, j);
+#pragma unroll
+            for (int k = 0; k < kBQ / 16; ++k)
+              mma_ts(tdV, tPa + k * 8, dOm + koff_mn(k), id_kv, (j > 0 || k > 0) ? 1u : 0u);
+          }
+          const uint64_t dX = sdesc_sw32(smem_u32(base + kOffX + st * 2 * kXBytes));
+          if (i < nq) {
+            issuer_wait(&bar.q_full[st], (i / kStages) & 1);
+            tc_fence_after();
+            const uint64_t dQk = sdesc_sw128(smem_u32(base + kOffQ + st * kQBytes), 16, 1024);
+            TRACE(T_ISS_S, i);
+#pragma unroll
+            for (int k = 0; k < D / 16; ++k) mma_ts(tS, tK + k * 8, dQk + koff_q(k), id_sdp, k > 0);
+            mma_ss(tS, dOnes, dX, id_sdp, 1u);
+            mma_commit(&bar.sdp_full);
+          }
+          if (i > 0) {
+            issuer_wait(&bar.pds_full, j & 1);
+            tc_fence_after();
+            const uint64_t dQm = sdesc_sw128(smem_u32(base + kOffQ + sj * kQBytes), kQPanel, 1024);
+            TRACE(T_ISS_DK, j);
+#pragma unroll
+            for (int k = 0; k < kBQ / 16; ++k)
+              mma_ts(tdK, tDSa + k * 8, dQm + koff_mn(k), id_kv, (j > 0 || k > 0) ? 1u : 0u);
+            mma_commit(&bar.q_empty[sj]);
+          }
+          if (i < nq) {
+            const uint64_t dOk = sdesc_sw128(smem_u32(base + kOffDO + st * kQBytes), 16, 1024);
+            TRACE(T_ISS_DP, i);
+#pragma unroll
+            for (int k = 0; k < D / 16; ++k) mma_ss(tdP, dVk + koff_kv(k), dOk + koff_q(k), id_sdp, k > 0);
+            mma_ss(tdP, dOnes, dX + (kXBytes >> 4), id_sdp, 1u);
+            mma_commit(&bar.dp_full);
+          }
+          if (i > 0) {
+            issuer_wait(&bar.dq_empty, (j & 1) ^ 1);
+            tc_fence_after();
+            TRACE(T_ISS_DQ, j);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) mma_ss(tdQ, dKt + koff_mn(k), dDS + koff_mn(k), id_dq, k > 0);
+            mma_commit(&bar.dq_full);
+            mma_commit(&bar.pds_empty);  // the dS^T shared-memory tile is free
+          }
+        }
+      }
+      for (int i = 0; i <= nq && !kKT; ++i) {
         if (i < nq) {
           const int st = i % kStages;
           issuer_wait(&bar.q_full[st], (i / kStages) & 1);
@@ -430,6 +501,25 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const int key = kbase + r;  // region-local key index
     uint8_t* sDS = base + kOffDS;
+    if constexpr (kKT) {
+      // K row r -> TMEM [128,192) (A operand of S^T): this warp's head-dim half = 32 columns
+      mbar_wait(&bar.kv_full, 0);
+      const int hh = warp >> 2;
+      const uint8_t* kp = base + kOffK + hh * kKVPanel;
+      uint32_t u[32];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 v = *reinterpret_cast<const uint4*>(kp + sw128_offset(r, c));
+        u[4 * c] = v.x;
+        u[4 * c + 1] = v.y;
+        u[4 * c + 2] = v.z;
+        u[4 * c + 3] = v.w;
+      }
+      tmem_st32(tmem + lane_off + 128 + hh * 32, u);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&bar.k_tm);
+    }
     QIter it;
     it.begin(cu, p.tq, s0, s1, tok_first);
     for (int i = 0; it.valid(); it.next(), ++i) {
@@ -437,6 +527,81 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
       mbar_wait(&bar.q_full[st], (i / kStages) & 1);
       mbar_wait(&bar.sdp_full, i & 1);
       tc_fence_after();
+      if constexpr (kKT) {
+        // P^T first (-> S^T's own columns, reported on p_ready), then dS^T once dP^T is complete
+        uint32_t us[32];
+        tmem_ld32(tmem + lane_off + c0, us);
+        tmem_wait_ld();
+        if (threadIdx.x == 0) TRACE(T_C_S, i);
+        int cmin;
+        if (!causal) {
+          cmin = key < kv_len ? 0 : kBQ;
+        } else {
+          const int dt = key - it.tok;
+          cmin = dt <= 0 ? 0 : min(dt * G, kBQ);
+        }
+        const int cmax = min(qrows, (it.rlen - it.tok) * G);
+        const float2 sl2 = make_float2(p.scale_log2, p.scale_log2);
+        uint32_t pp[16];
+        auto math_p = [&](auto masked) {
+#pragma unroll
+          for (int c2 = 0; c2 < 16; ++c2) {
+            const float2 x =
+                __fmul2_rn(make_float2(__uint_as_float(us[2 * c2]), __uint_as_float(us[2 * c2 + 1])), sl2);
+            float2 e;
+            if (c2 >= 16 - kPolyPairs) {
+              e = ex2_poly2(x);
+            } else {
+              e.x = ex2(x.x);
+              e.y = ex2(x.y);
+            }
+            if constexpr (decltype(masked)::value) {
+              const int c = c0 + 2 * c2;
+              e.x = (c >= cmin && c < cmax) ? e.x : 0.f;
+              e.y = (c + 1 >= cmin && c + 1 < cmax) ? e.y : 0.f;
+            }
+            us[2 * c2] = __float_as_uint(e.x);
+            us[2 * c2 + 1] = __float_as_uint(e.y);
+            pp[c2] = pack_bf16(e.x, e.y);
+          }
+        };
+        if (__all_sync(0xffffffffu, cmin <= c0 && cmax >= c0 + 32))
+          math_p(std::false_type{});
+        else
+          math_p(std::true_type{});
+        tmem_st16(tmem + lane_off + 16 + c0 / 2, pp);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bar.p_ready);
+        if (threadIdx.x == 0) TRACE(T_C_P, i);
+        mbar_wait(&bar.dp_full, i & 1);
+        tc_fence_after();
+        uint32_t ud[32];
+        tmem_ld32(tmem + lane_off + 64 + c0, ud);
+        tmem_wait_ld();
+        if (threadIdx.x == 0) TRACE(T_C_DP, i);
+        uint32_t pd[16];
+#pragma unroll
+        for (int c2 = 0; c2 < 16; ++c2) {
+          const float2 dd = __fmul2_rn(make_float2(__uint_as_float(us[2 * c2]), __uint_as_float(us[2 * c2 + 1])),
+                                       make_float2(__uint_as_float(ud[2 * c2]), __uint_as_float(ud[2 * c2 + 1])));
+          pd[c2] = pack_bf16(dd.x, dd.y);
+        }
+        mbar_wait(&bar.pds_empty, (i & 1) ^ 1);  // dQ^T(i-1) is done with the dS^T tile in smem
+        tc_fence_after();
+        tmem_st16(tmem + lane_off + 80 + c0 / 2, pd);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          const uint32_t off = sw128_offset(r, c0 / 8 + ch);
+          *reinterpret_cast<uint4*>(sDS + off) = make_uint4(pd[4 * ch], pd[4 * ch + 1], pd[4 * ch + 2], pd[4 * ch + 3]);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        fence_async_smem();
+        mbar_arrive(&bar.pds_full);
+        if (threadIdx.x == 0) TRACE(T_C_DS, i);
+        continue;
+      }
       if (threadIdx.x == 0) TRACE(T_C_S, i);
       uint32_t us[32], ud[32];
       tmem_ld32(tmem + lane_off + c0, us);
