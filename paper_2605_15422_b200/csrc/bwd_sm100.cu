@@ -372,6 +372,8 @@ __global__ void __launch_bounds__(kThreads, 1) dualkv_bwd_kernel(const __grid_co
           mbar_spin(b, ph);
         else if constexpr (BWD_SPIN == 2)
           mbar_wait_nohint(b, ph);
+        else if constexpr (BWD_SPIN >= 16)  // a short suspend-time hint of BWD_SPIN ns
+          mbar_wait_hint<BWD_SPIN>(b, ph);
         else
           mbar_wait(b, ph);
       };

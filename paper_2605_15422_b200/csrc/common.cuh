@@ -160,6 +160,21 @@ DKV_DEVICE void mbar_wait_nohint(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// try_wait with a short suspend-time hint (ns): the thread re-checks at least that often
+template <int kNs>
+DKV_DEVICE void mbar_wait_hint(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "n"(kNs)
+        : "memory");
+  }
+}
+
 // generic-proxy smem writes -> visible to the async proxy (UMMA / TMA reads)
 DKV_DEVICE void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
